@@ -1,0 +1,136 @@
+/*
+ * quartet_b200.h -- C ABI of the B200-native Quartet linear-layer hot path (libquartet_b200.so).
+ *
+ * Drop-in boundary for the reference's operator-plugin seam: the duck-typed `kernels` backend
+ * module of mx4train (/root/reference/pkg/src/mx4train/_backend/__init__.py:13-35) whose entry
+ * points are quantize_rtn / quantize_sr / quantize_quest / fwht / gemm_nt
+ * (_backend/_native.pyx:104-396), composed by qlinear.forward / qlinear.backward
+ * (qlinear.py:114-252).  Each entry point below cites the reference interface it replaces.
+ *
+ * Conventions (all functions):
+ *   - plain device pointers, sizes in elements unless a name says bytes; no allocation, no throw;
+ *   - stream-ordered on the caller's `stream` (a cudaStream_t passed as void*); reentrant, no
+ *     global mutable state beyond a lazily resolved driver entry point;
+ *   - return 0 on success, a cudaError_t value (1..999) on a CUDA error, or a QT_ERR_* code;
+ *   - `err` (nullable, device int) gets bit 0 set when a quantizer sees a non-finite input: the
+ *     analogue of the reference's ValueError("non-finite input") (codec.py:164-170), checked by
+ *     the host wrapper after the call;
+ *   - every quantized axis length must be a multiple of 32 (the reference requires the same on the
+ *     layer path: qlinear.py:136-137, 200-204).
+ *
+ * MXFP4 operand layout (one [R, K] matrix quantized in groups of 32 along K):
+ *   codes  uint8 [R, K/2], element 2k in the low nibble of byte k (== reference pack_nibbles,
+ *          codec.py:146-153, so `codes` bytes equal QuantizedTensor.codes bytes)
+ *   sf     uint8 E8M0 scale bytes (== QuantizedTensor.scales values) in tcgen05 scale atoms:
+ *          byte offset of (row r, group g) = ((r/128)*katoms + g/4)*512 + (r%32)*16
+ *                                            + ((r%128)/32)*4 + g%4
+ *          with katoms = qt_sf_katoms(K); buffer size qt_sf_bytes(R, K), zero-initialised by the
+ *          caller (padding must hold a finite exponent).
+ *   mask   uint32 [R, K/32], bit j of word (r, g): |x/s| <= 6 at the chosen scale (LayerContext
+ *          m_x / m_w, qlinear.py:74-87, as a bitmap instead of a bool matrix).
+ */
+#ifndef QUARTET_B200_H
+#define QUARTET_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define QT_API __attribute__((visibility("default")))
+#else
+#define QT_API
+#endif
+
+#define QT_ABI_VERSION 1
+
+/* error codes beyond cudaError_t */
+#define QT_ERR_SHAPE 2001  /* axis not a multiple of 32 / mismatched operands (ValueError upstream) */
+#define QT_ERR_ALIGN 2002  /* pointer or leading dimension not 16-byte aligned */
+#define QT_ERR_ARG 2003    /* unknown enum value */
+#define QT_ERR_TMA 2004    /* tensor-map creation failed */
+
+/* dtype / mode enums */
+#define QT_IN_BF16 0
+#define QT_IN_F32 1
+#define QT_IN_MXFP4 2
+#define QT_TRANSFORM_NONE 0        /* no rotation */
+#define QT_TRANSFORM_HADAMARD 1    /* hadamard.transform_last_axis, g = 32 (hadamard.py:72-74) */
+#define QT_TRANSFORM_RANDOMIZED 2  /* randomized_transform_last_axis (hadamard.py:82-85) */
+#define QT_ROUND_QUEST 0           /* quantize_quest, ratio_lo = 1/16 (_native.pyx:206-245) */
+#define QT_ROUND_RTN 1             /* quantize_rtn (_native.pyx:104-131) */
+#define QT_ROUND_SR 2              /* quantize_sr (_native.pyx:134-168) */
+#define QT_EPI_STORE 0             /* D = A B^T */
+#define QT_EPI_MASK_H 1            /* D = H32(A B^T (.) mask) * scale (qlinear.py:229-230, 249-250) */
+#define QT_EPI_MASK 2              /* D = (A B^T (.) mask) * scale (hadamard=False layers) */
+#define QT_OUT_F32 0
+#define QT_OUT_BF16 1
+
+QT_API int qt_abi_version(void);
+QT_API const char* qt_error_string(int code);
+
+/* ---- geometry helpers (host) */
+QT_API int64_t qt_codes_ld(int64_t k);            /* bytes per codes row: k/2 */
+QT_API int64_t qt_sf_katoms(int64_t k);           /* scale atoms per 128-row block: 2*ceil(k/256) */
+QT_API int64_t qt_sf_bytes(int64_t rows, int64_t k);
+
+/* ---- counter RNG (host), rng.py:27-78 */
+QT_API uint64_t qt_mix64(uint64_t z);                                   /* rng.mix64 */
+QT_API uint64_t qt_derive_seed(const uint64_t* parts, int nparts);      /* rng.derive_seed */
+
+/* Sign bitmap of rng.signs(xi, 0, n) (rng.py:57-62): bit p%32 of word p/32 is 1 where the
+ * randomized Hadamard flips position p.  d_bits holds ceil(n/32) words. */
+QT_API int qt_sign_bits(uint32_t* d_bits, int64_t n, uint64_t xi, void* stream);
+
+/* ---- general quantizers ---------------------------------------------------------------
+ * qt_quant_rows: groups along the contiguous axis of x[rows, cols] (row stride ldx elements).
+ *   transform (+ sign_bits for RANDOMIZED, indexed by column), then * prescale (1.0 or 0.75,
+ *   qlinear.py:219-220), then quantize with `rounding` (SR: seed = per-tensor seed, stream
+ *   position counter_start + r*cols + c, quantizers.py:79-84).
+ *   Replaces: kernels.fwht + kernels.quantize_{quest,rtn,sr} on a row-major matrix. */
+QT_API int qt_quant_rows(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_t cols, int transform,
+                  const uint32_t* sign_bits, float prescale, int rounding, uint64_t sr_seed, uint64_t counter_start,
+                  uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, uint32_t* mask, int* err,
+                  int* fallbacks, void* stream);
+
+/* qt_quant_cols: quantize the TRANSPOSE of x[rows, cols]: output operand [cols, rows] with groups
+ *   along `rows`; sign_bits indexed by row; SR stream position counter_start + c*rows + r.
+ *   in_dtype QT_IN_MXFP4 reads x as an MXFP4 operand (mx_codes/mx_ldc/mx_sf/mx_katoms; x unused)
+ *   and dequantizes it exactly first (qlinear._values, qlinear.py:90-93). */
+QT_API int qt_quant_cols(const void* x, int in_dtype, int64_t ldx, const uint8_t* mx_codes, int64_t mx_ldc,
+                  const uint8_t* mx_sf, int64_t mx_katoms, int64_t rows, int64_t cols, int transform,
+                  const uint32_t* sign_bits, float prescale, int rounding, uint64_t sr_seed, uint64_t counter_start,
+                  uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, int* err, void* stream);
+
+/* ---- named hot-path entry points (dense row-major inputs, ld == cols) ------------------- */
+
+/* Forward operand quantizer: x_h = H32(x) (if hadamard), QuEST -> codes/sf/mask.
+ * Replaces qlinear.py:139-141 + apply_scheme(x_h, QUEST) (quantizers.py:87-92). */
+QT_API int qt_quant_fwd_quest(const void* x, int in_dtype, int64_t rows, int64_t cols, int hadamard, uint8_t* codes,
+                       uint8_t* sf, uint32_t* mask, int* err, void* stream);
+
+/* Backward row operand: Q(H32(dy (.) s_xi) * 0.75) along d_out (qlinear.py:214, 219, 225). */
+QT_API int qt_quant_bwd_rows(const void* dy, int in_dtype, int64_t rows, int64_t cols, const uint32_t* sign_bits,
+                      int rounding, uint64_t sr_seed, uint8_t* codes, uint8_t* sf, int* err, void* stream);
+
+/* Backward transposed operand: Q(H32(dy^T (.) s_xi) * 0.75) along tokens (qlinear.py:234, 239, 245). */
+QT_API int qt_quant_bwd_cols(const void* dy, int in_dtype, int64_t rows, int64_t cols, const uint32_t* sign_bits,
+                      int rounding, uint64_t sr_seed, uint8_t* codes, uint8_t* sf, int* err, void* stream);
+
+/* Requant-transpose of a saved MXFP4 operand [rows, cols]:
+ * Q(H32(deq(q)^T (.) s_xi) * 0.75) -> operand [cols, rows] (qlinear.py:206-207, 215, 235). */
+QT_API int qt_requant_t(const uint8_t* codes, const uint8_t* sf, int64_t rows, int64_t cols, const uint32_t* sign_bits,
+                 int rounding, uint64_t sr_seed, uint8_t* out_codes, uint8_t* out_sf, int* err, void* stream);
+
+/* MXFP4 GEMM D[M,N] = deq(A)[M,K] deq(B)[N,K]^T on tcgen05 (gemm_lp, qlinear.py:96-111), with an
+ * optional fused epilogue (QT_EPI_MASK_H: mask[M, N/32], FWHT-32 along N, * scale). */
+QT_API int qt_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b_codes, const uint8_t* b_sf,
+                 int64_t M, int64_t N, int64_t K, void* out, int out_dtype, int64_t ldo, int epilogue,
+                 const uint32_t* mask, float scale, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

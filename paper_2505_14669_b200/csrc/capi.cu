@@ -1,0 +1,128 @@
+// capi.cu -- extern "C" boundary of libquartet_b200.so (declared in include/quartet_b200.h).
+#include "../../include/quartet_b200.h"
+#include "common.cuh"
+
+#include "launch.h"
+
+using namespace qt;
+
+static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+static inline uint64_t sr_base_of(uint64_t seed) { return mix64(seed ^ mix64(kDomainSR)); }
+
+extern "C" {
+
+int qt_abi_version(void) { return QT_ABI_VERSION; }
+
+const char* qt_error_string(int code) {
+    switch (code) {
+        case 0: return "ok";
+        case QT_ERR_SHAPE: return "shape: quantized axis not a multiple of 32 or operand mismatch";
+        case QT_ERR_ALIGN: return "alignment: pointer or leading dimension not 16-byte aligned";
+        case QT_ERR_ARG: return "bad enum argument";
+        case QT_ERR_TMA: return "tensor map creation failed";
+        default: return cudaGetErrorString((cudaError_t)code);
+    }
+}
+
+int64_t qt_codes_ld(int64_t k) { return k / 2; }
+int64_t qt_sf_katoms(int64_t k) { return 2 * ((k + 255) / 256); }
+int64_t qt_sf_bytes(int64_t rows, int64_t k) { return ((rows + 255) / 256) * 2 * qt_sf_katoms(k) * 512; }
+
+uint64_t qt_mix64(uint64_t z) { return mix64(z); }
+
+uint64_t qt_derive_seed(const uint64_t* parts, int nparts) {
+    uint64_t acc = 0x243F6A8885A308D3ULL;
+    for (int i = 0; i < nparts; ++i) {
+        acc = mix64(acc ^ parts[i]);
+        acc = acc + kGolden;
+    }
+    return mix64(acc);
+}
+
+int qt_sign_bits(uint32_t* d_bits, int64_t n, uint64_t xi, void* stream) {
+    return launch_signs(d_bits, n, xi, (cudaStream_t)stream);
+}
+
+int qt_quant_rows(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_t cols, int transform,
+                  const uint32_t* sign_bits, float prescale, int rounding, uint64_t sr_seed, uint64_t counter_start,
+                  uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, uint32_t* mask, int* err, int* fallbacks,
+                  void* stream) {
+    if (cols % 32 != 0 || rows < 0) return QT_ERR_SHAPE;
+    if (in_dtype != QT_IN_BF16 && in_dtype != QT_IN_F32) return QT_ERR_ARG;
+    if (rounding < 0 || rounding > 2 || transform < 0 || transform > 2) return QT_ERR_ARG;
+    if (transform == QT_TRANSFORM_RANDOMIZED && !sign_bits) return QT_ERR_ARG;
+    int esz = in_dtype == QT_IN_BF16 ? 2 : 4;
+    if (!al16(x) || (ldx * esz) % 16 || !al16(codes) || ldc % 16) return QT_ERR_ALIGN;
+    QuantCfg cfg{transform, sign_bits, prescale, rounding, sr_base_of(sr_seed), counter_start};
+    QuantOut out{codes, ldc, sf, katoms, mask, err, fallbacks};
+    return launch_quant_rows(x, in_dtype, ldx, rows, cols, cfg, out, (cudaStream_t)stream);
+}
+
+int qt_quant_cols(const void* x, int in_dtype, int64_t ldx, const uint8_t* mx_codes, int64_t mx_ldc,
+                  const uint8_t* mx_sf, int64_t mx_katoms, int64_t rows, int64_t cols, int transform,
+                  const uint32_t* sign_bits, float prescale, int rounding, uint64_t sr_seed, uint64_t counter_start,
+                  uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, int* err, void* stream) {
+    if (rows % 32 != 0 || cols % 32 != 0) return QT_ERR_SHAPE;
+    if (in_dtype < 0 || in_dtype > 2 || rounding < 0 || rounding > 2 || transform < 0 || transform > 2)
+        return QT_ERR_ARG;
+    if (transform == QT_TRANSFORM_RANDOMIZED && !sign_bits) return QT_ERR_ARG;
+    if (in_dtype == QT_IN_MXFP4) {
+        if (!al16(mx_codes) || mx_ldc % 16) return QT_ERR_ALIGN;
+    } else {
+        int esz = in_dtype == QT_IN_BF16 ? 2 : 4;
+        if (!al16(x) || (ldx * esz) % 16) return QT_ERR_ALIGN;
+    }
+    if (!al16(codes) || ldc % 16) return QT_ERR_ALIGN;
+    QuantCfg cfg{transform, sign_bits, prescale, rounding, sr_base_of(sr_seed), counter_start};
+    QuantOut out{codes, ldc, sf, katoms, nullptr, err, nullptr};
+    MxIn mx{mx_codes, mx_ldc, mx_sf, mx_katoms};
+    return launch_quant_cols(x, in_dtype, ldx, mx, rows, cols, cfg, out, (cudaStream_t)stream);
+}
+
+int qt_quant_fwd_quest(const void* x, int in_dtype, int64_t rows, int64_t cols, int hadamard, uint8_t* codes,
+                       uint8_t* sf, uint32_t* mask, int* err, void* stream) {
+    return qt_quant_rows(x, in_dtype, cols, rows, cols, hadamard ? QT_TRANSFORM_HADAMARD : QT_TRANSFORM_NONE, nullptr,
+                         1.0f, QT_ROUND_QUEST, 0, 0, codes, qt_codes_ld(cols), sf, qt_sf_katoms(cols), mask, err,
+                         nullptr, stream);
+}
+
+int qt_quant_bwd_rows(const void* dy, int in_dtype, int64_t rows, int64_t cols, const uint32_t* sign_bits,
+                      int rounding, uint64_t sr_seed, uint8_t* codes, uint8_t* sf, int* err, void* stream) {
+    if (rounding == QT_ROUND_QUEST) return QT_ERR_ARG;
+    return qt_quant_rows(dy, in_dtype, cols, rows, cols, sign_bits ? QT_TRANSFORM_RANDOMIZED : QT_TRANSFORM_NONE,
+                         sign_bits, 0.75f, rounding, sr_seed, 0, codes, qt_codes_ld(cols), sf, qt_sf_katoms(cols),
+                         nullptr, err, nullptr, stream);
+}
+
+int qt_quant_bwd_cols(const void* dy, int in_dtype, int64_t rows, int64_t cols, const uint32_t* sign_bits,
+                      int rounding, uint64_t sr_seed, uint8_t* codes, uint8_t* sf, int* err, void* stream) {
+    if (rounding == QT_ROUND_QUEST) return QT_ERR_ARG;
+    return qt_quant_cols(dy, in_dtype, cols, nullptr, 0, nullptr, 0, rows, cols,
+                         sign_bits ? QT_TRANSFORM_RANDOMIZED : QT_TRANSFORM_NONE, sign_bits, 0.75f, rounding, sr_seed,
+                         0, codes, qt_codes_ld(rows), sf, qt_sf_katoms(rows), err, stream);
+}
+
+int qt_requant_t(const uint8_t* codes, const uint8_t* sf, int64_t rows, int64_t cols, const uint32_t* sign_bits,
+                 int rounding, uint64_t sr_seed, uint8_t* out_codes, uint8_t* out_sf, int* err, void* stream) {
+    if (rounding == QT_ROUND_QUEST) return QT_ERR_ARG;
+    return qt_quant_cols(nullptr, QT_IN_MXFP4, 0, codes, qt_codes_ld(cols), sf, qt_sf_katoms(cols), rows, cols,
+                         sign_bits ? QT_TRANSFORM_RANDOMIZED : QT_TRANSFORM_NONE, sign_bits, 0.75f, rounding, sr_seed,
+                         0, out_codes, qt_codes_ld(rows), out_sf, qt_sf_katoms(rows), err, stream);
+}
+
+int qt_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b_codes, const uint8_t* b_sf, int64_t M,
+                 int64_t N, int64_t K, void* out, int out_dtype, int64_t ldo, int epilogue, const uint32_t* mask,
+                 float scale, void* stream) {
+    if (K % 32 != 0 || K <= 0 || N % 32 != 0 || M < 0) return QT_ERR_SHAPE;
+    if (epilogue < QT_EPI_STORE || epilogue > QT_EPI_MASK) return QT_ERR_ARG;
+    if (out_dtype != QT_OUT_F32 && out_dtype != QT_OUT_BF16) return QT_ERR_ARG;
+    if (epilogue != QT_EPI_STORE && !mask) return QT_ERR_ARG;
+    int esz = out_dtype == QT_OUT_BF16 ? 2 : 4;
+    if (!al16(a_codes) || !al16(b_codes) || !al16(out) || (ldo * esz) % 16) return QT_ERR_ALIGN;
+    EpiParams ep{out, ldo, out_dtype == QT_OUT_BF16, epilogue, mask, N / 32, scale};
+    int rc = launch_gemm(a_codes, qt_codes_ld(K), a_sf, qt_sf_katoms(K), b_codes, qt_codes_ld(K), b_sf,
+                         qt_sf_katoms(K), M, N, K, ep, (cudaStream_t)stream);
+    return rc == 1001 || rc == 1002 ? QT_ERR_TMA : rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// launch.h -- host-side launcher interface shared by the kernel TUs and the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qt {
+
+enum InType : int { kInBF16 = 0, kInF32 = 1, kInMXFP4 = 2 };
+enum Transform : int { kNone = 0, kHadamard = 1, kRandomized = 2 };
+enum EpiMode : int { kEpiStore = 0, kEpiMaskH = 1, kEpiMask = 2 };
+
+struct QuantOut {
+    uint8_t* codes;
+    int64_t ldc;      // bytes per output row
+    uint8_t* sf;
+    int64_t katoms;   // scale-factor atoms per 128-row block
+    uint32_t* mask;   // nullable; [rows, K/32]
+    int* err;         // nullable; bit 0 = non-finite input seen
+    int* fallbacks;   // nullable; QuEST exact-search count
+};
+
+struct QuantCfg {
+    int transform;
+    const uint32_t* sign_bits;  // bit p%32 of word p/32 = 1 -> flip sign at axis position p
+    float prescale;             // 1.0 or 0.75
+    int rounding;
+    uint64_t sr_base;           // mix64(seed ^ mix64(DOMAIN_SR))
+    uint64_t counter_start;
+};
+
+struct MxIn {
+    const uint8_t* codes;
+    int64_t ldc;
+    const uint8_t* sf;
+    int64_t katoms;
+};
+
+struct EpiParams {
+    void* out;
+    int64_t ldo;             // elements
+    int out_bf16;
+    int mode;
+    const uint32_t* mask;    // [M, N/32] words (kEpiMaskH)
+    int64_t ldm;             // words per mask row
+    float scale;
+};
+
+int launch_signs(uint32_t* bits, int64_t n, uint64_t xi, cudaStream_t st);
+int launch_quant_rows(const void* x, int in_type, int64_t ldx, int64_t rows, int64_t cols, const QuantCfg& cfg,
+                      const QuantOut& out, cudaStream_t st);
+int launch_quant_cols(const void* x, int in_type, int64_t ldx, const MxIn& mx, int64_t R, int64_t C,
+                      const QuantCfg& cfg, const QuantOut& out, cudaStream_t st);
+int launch_gemm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, int64_t a_katoms, const uint8_t* b, int64_t ldb,
+                const uint8_t* b_sf, int64_t b_katoms, int64_t M, int64_t N, int64_t K, const EpiParams& ep,
+                cudaStream_t st);
+
+}  // namespace qt

@@ -1,0 +1,178 @@
+"""Device-resident MXFP4 operands and the thin torch wrappers around the C ABI.
+
+An ``MXOperand`` is the B200 form of the reference's ``QuantizedTensor`` (codec.py:39-72): the
+same packed code bytes (element 2k in the low nibble), the same E8M0 exponent values, but the
+scales live in tcgen05 scale-factor atoms (see include/quartet_b200.h) so the GEMM can stage them
+straight into tensor memory.  ``scales_rowmajor()`` recovers the reference's [rows, cols/32]
+``scales`` matrix for parity checks.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import check
+
+GROUP = 32
+
+
+def _stream(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _require_cuda(t: torch.Tensor, name: str) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (the Quartet B200 path has no CPU fallback)")
+
+
+@dataclass
+class MXOperand:
+    codes: torch.Tensor          # uint8 [rows, cols/2]
+    sf: torch.Tensor             # uint8 scale atoms, qt_sf_bytes(rows, cols)
+    rows: int
+    cols: int
+    mask: torch.Tensor | None = None   # int32 [rows, cols/32] bitmap (QuEST trust mask)
+
+    @property
+    def shape(self):
+        return (self.rows, self.cols)
+
+    @property
+    def katoms(self) -> int:
+        return 2 * ((self.cols + 255) // 256)
+
+    @staticmethod
+    def empty(rows: int, cols: int, device, with_mask: bool = False) -> "MXOperand":
+        L = _lib.load()
+        if cols % GROUP:
+            raise ValueError(f"axis length {cols} not divisible by block size {GROUP}")
+        codes = torch.empty((rows, cols // 2), dtype=torch.uint8, device=device)
+        sf = torch.zeros(int(L.qt_sf_bytes(rows, cols)), dtype=torch.uint8, device=device)
+        mask = torch.empty((rows, cols // GROUP), dtype=torch.int32, device=device) if with_mask else None
+        return MXOperand(codes, sf, rows, cols, mask)
+
+    # ---------------------------------------------------------------- parity helpers
+    def scales_rowmajor(self) -> torch.Tensor:
+        """uint8 [rows, cols/32] in the reference layout (QuantizedTensor.scales)."""
+        r = torch.arange(self.rows, device=self.sf.device).view(-1, 1)
+        g = torch.arange(self.cols // GROUP, device=self.sf.device).view(1, -1)
+        off = ((r >> 7) * self.katoms + (g >> 2)) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (g & 3)
+        return self.sf[off]
+
+    def mask_bool(self) -> torch.Tensor:
+        """bool [rows, cols]: the reference's m_x / m_w."""
+        bits = torch.arange(32, device=self.codes.device, dtype=torch.int64)
+        m = (self.mask.to(torch.int64).unsqueeze(-1) >> bits) & 1
+        return m.reshape(self.rows, self.cols).bool()
+
+    def unpacked_codes(self) -> torch.Tensor:
+        c = self.codes
+        return torch.stack([c & 0x0F, c >> 4], dim=-1).reshape(self.rows, self.cols)
+
+    def dequantize(self, dtype=torch.float32) -> torch.Tensor:
+        """Exact code * 2^(e-127) (codec.py:204-211); parity/debug helper, not on the hot path."""
+        grid = torch.tensor([0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0], dtype=torch.float64, device=self.codes.device)
+        dec = torch.cat([grid, -grid])
+        vals = dec[self.unpacked_codes().long()]
+        s = torch.ldexp(torch.ones((), dtype=torch.float64, device=self.codes.device),
+                        self.scales_rowmajor().to(torch.int64) - 127)
+        return (vals * s.repeat_interleave(GROUP, dim=1)).to(dtype)
+
+
+# ------------------------------------------------------------------------ C-ABI calls
+
+def _in_dtype(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return _lib.QT_IN_BF16
+    if t.dtype == torch.float32:
+        return _lib.QT_IN_F32
+    raise ValueError(f"unsupported input dtype {t.dtype} (bf16 or fp32)")
+
+
+def derive_seed(*parts: int) -> int:
+    """rng.derive_seed (rng.py:72-78), computed by the library."""
+    import ctypes
+
+    arr = (ctypes.c_uint64 * len(parts))(*[int(p) & 0xFFFFFFFFFFFFFFFF for p in parts])
+    return int(_lib.load().qt_derive_seed(ctypes.cast(arr, ctypes.c_void_p), len(parts)))
+
+
+def sign_bits(xi: int, n: int, device) -> torch.Tensor:
+    """Device bitmap of rng.signs(xi, 0, n): int32 [ceil(n/32)]."""
+    out = torch.empty(((n + 31) // 32,), dtype=torch.int32, device=device)
+    check(_lib.load().qt_sign_bits(out.data_ptr(), n, int(xi) & 0xFFFFFFFFFFFFFFFF, _stream(out.device)),
+          "qt_sign_bits")
+    return out
+
+
+def quant_rows(x: torch.Tensor, transform: int, rounding: int, *, signs: torch.Tensor | None = None,
+               prescale: float = 1.0, sr_seed: int = 0, counter_start: int = 0, want_mask: bool = False,
+               err: torch.Tensor | None = None, fallbacks: torch.Tensor | None = None,
+               out: MXOperand | None = None) -> MXOperand:
+    _require_cuda(x, "x")
+    if x.dim() != 2:
+        raise ValueError("expected a 2-D matrix")
+    if x.stride(1) != 1:
+        x = x.contiguous()
+    rows, cols = x.shape
+    if cols % GROUP:
+        raise ValueError(f"axis length {cols} not divisible by block size {GROUP}")
+    op = out if out is not None else MXOperand.empty(rows, cols, x.device, with_mask=want_mask)
+    L = _lib.load()
+    rc = L.qt_quant_rows(x.data_ptr(), _in_dtype(x), x.stride(0), rows, cols, transform,
+                         signs.data_ptr() if signs is not None else None, float(prescale), rounding,
+                         int(sr_seed) & 0xFFFFFFFFFFFFFFFF, int(counter_start),
+                         op.codes.data_ptr(), op.codes.stride(0), op.sf.data_ptr(), op.katoms,
+                         op.mask.data_ptr() if op.mask is not None else None,
+                         err.data_ptr() if err is not None else None,
+                         fallbacks.data_ptr() if fallbacks is not None else None, _stream(x.device))
+    check(rc, "qt_quant_rows")
+    return op
+
+
+def quant_cols(x, rounding: int, *, transform: int, signs: torch.Tensor | None = None, prescale: float = 1.0,
+               sr_seed: int = 0, counter_start: int = 0, err: torch.Tensor | None = None,
+               out: MXOperand | None = None) -> MXOperand:
+    """Quantize the transpose of x ([rows, cols] dense tensor or MXOperand) along `rows`."""
+    L = _lib.load()
+    if isinstance(x, MXOperand):
+        rows, cols, dev = x.rows, x.cols, x.codes.device
+        args = (None, _lib.QT_IN_MXFP4, 0, x.codes.data_ptr(), x.codes.stride(0), x.sf.data_ptr(), x.katoms)
+    else:
+        _require_cuda(x, "x")
+        if x.stride(1) != 1:
+            x = x.contiguous()
+        rows, cols = x.shape
+        dev = x.device
+        args = (x.data_ptr(), _in_dtype(x), x.stride(0), None, 0, None, 0)
+    if rows % GROUP or cols % GROUP:
+        raise ValueError(f"transposed quantization needs both axes divisible by {GROUP}: {rows}x{cols}")
+    op = out if out is not None else MXOperand.empty(cols, rows, dev)
+    rc = L.qt_quant_cols(*args, rows, cols, transform, signs.data_ptr() if signs is not None else None,
+                         float(prescale), rounding, int(sr_seed) & 0xFFFFFFFFFFFFFFFF, int(counter_start),
+                         op.codes.data_ptr(), op.codes.stride(0), op.sf.data_ptr(), op.katoms,
+                         err.data_ptr() if err is not None else None, _stream(dev))
+    check(rc, "qt_quant_cols")
+    return op
+
+
+def gemm(a: MXOperand, b: MXOperand, *, out_dtype=torch.float32, mask: torch.Tensor | None = None,
+         hadamard: bool = True, scale: float = 1.0, out: torch.Tensor | None = None) -> torch.Tensor:
+    """deq(a) @ deq(b).T on tcgen05 (gemm_lp, qlinear.py:96-111); with `mask`, the fused
+    H32(D * mask) * scale epilogue (qlinear.py:229-230)."""
+    if a.cols != b.cols:
+        raise ValueError(f"contraction mismatch: {a.cols} vs {b.cols}")
+    M, N, K = a.rows, b.rows, a.cols
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype, device=a.codes.device)
+    odt = _lib.QT_OUT_BF16 if out.dtype == torch.bfloat16 else _lib.QT_OUT_F32
+    epi = _lib.QT_EPI_STORE if mask is None else (_lib.QT_EPI_MASK_H if hadamard else _lib.QT_EPI_MASK)
+    rc = _lib.load().qt_gemm_mxf4(a.codes.data_ptr(), a.sf.data_ptr(), b.codes.data_ptr(), b.sf.data_ptr(),
+                                  M, N, K, out.data_ptr(), odt, out.stride(0), epi,
+                                  mask.data_ptr() if mask is not None else None, float(scale),
+                                  _stream(out.device))
+    check(rc, "qt_gemm_mxf4")
+    return out

@@ -1,0 +1,86 @@
+"""torch.autograd.Function / nn.Module surface of the Quartet linear layer.
+
+``QuartetLinearFn`` is the drop-in autograd form of the reference's functional pair
+(qlinear.forward / qlinear.backward, qlinear.py:114-252): its ctx carries the reference's
+LayerContext (quantized X/W operands and trust masks), ``xi`` seeds the backward randomized
+Hadamard / stochastic rounding, and ``rounding`` selects "rtn" (default) or "sr".
+
+``QuartetLinear`` is a bias-free linear module (the reference's layers are bias-free,
+qlinear.py:18) holding an fp32 master weight; it derives a fresh ``xi`` per step the way the
+reference's training loop does (train.py:346-348: derive_seed(derive_seed(seed, 4, step), layer)).
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import qlinear
+from .mxfp4 import derive_seed
+
+
+class QuartetLinearFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, xi: int, rounding: str = "rtn", hadamard: bool = True,
+                scheme: qlinear.QuantScheme = qlinear.QUEST):
+        lead = x.shape[:-1]
+        x2 = x.reshape(-1, x.shape[-1])
+        if x2.dtype not in (torch.bfloat16, torch.float32):
+            x2 = x2.float()
+        y, lctx = qlinear.forward(x2, w.detach(), scheme=scheme, hadamard=hadamard, seed=xi,
+                                  out_dtype=x.dtype if x.dtype in (torch.bfloat16, torch.float32) else torch.float32,
+                                  check_finite=False)
+        ctx.lctx = lctx
+        ctx.xi = int(xi)
+        ctx.rounding = rounding
+        ctx.x_shape = x.shape
+        ctx.x_dtype = x.dtype
+        ctx.w_dtype = w.dtype
+        return y.reshape(*lead, w.shape[0])
+
+    @staticmethod
+    def backward(ctx, dy):
+        dy2 = dy.reshape(-1, dy.shape[-1])
+        if dy2.dtype not in (torch.bfloat16, torch.float32):
+            dy2 = dy2.float()
+        dx, dw = qlinear.backward(dy2, ctx.lctx, ctx.xi, ctx.rounding, dx_dtype=ctx.x_dtype
+                                  if ctx.x_dtype in (torch.bfloat16, torch.float32) else torch.float32,
+                                  dw_dtype=torch.float32, check_finite=False)
+        ctx.lctx = None
+        return dx.reshape(ctx.x_shape), dw.to(ctx.w_dtype), None, None, None, None
+
+
+def quartet_linear(x, w, xi: int, rounding: str = "rtn", hadamard: bool = True,
+                   scheme: qlinear.QuantScheme = qlinear.QUEST):
+    return QuartetLinearFn.apply(x, w, xi, rounding, hadamard, scheme)
+
+
+class QuartetLinear(torch.nn.Module):
+    """Bias-free MXFP4 linear layer (Quartet Alg. 1) with an fp32 master weight."""
+
+    def __init__(self, in_features: int, out_features: int, *, seed: int = 0, layer_id: int = 0,
+                 rounding: str = "rtn", hadamard: bool = True, scheme: qlinear.QuantScheme = qlinear.QUEST,
+                 device=None, dtype=torch.float32):
+        super().__init__()
+        if in_features % 32 or out_features % 32:
+            raise ValueError("Quartet linear dimensions must be multiples of 32")
+        self.in_features, self.out_features = in_features, out_features
+        self.weight = torch.nn.Parameter(torch.empty(out_features, in_features, device=device, dtype=dtype))
+        self.seed, self.layer_id = int(seed), int(layer_id)
+        self.rounding, self.hadamard, self.scheme = rounding, hadamard, scheme
+        self.step = 0
+        torch.nn.init.normal_(self.weight, std=1.0 / math.sqrt(in_features))
+
+    def xi(self) -> int:
+        return derive_seed(derive_seed(self.seed, 4, self.step), self.layer_id)
+
+    def forward(self, x):
+        xi = self.xi()
+        if self.training:
+            self.step += 1
+        return QuartetLinearFn.apply(x, self.weight, xi, self.rounding, self.hadamard, self.scheme)
+
+    def extra_repr(self) -> str:
+        return (f"in_features={self.in_features}, out_features={self.out_features}, "
+                f"scheme={self.scheme.kind}, rounding={self.rounding}, hadamard={self.hadamard}")

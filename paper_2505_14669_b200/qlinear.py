@@ -1,0 +1,220 @@
+"""Quartet linear layer (Alg. 1) on B200: the functional forward / backward pair.
+
+Mirrors the reference's layer seam one-to-one (mx4train/qlinear.py):
+
+    forward(x, w, scheme=QUEST, policy=DEFAULT_POLICY, hadamard=True, seed=None) -> (y, LayerContext)
+        qlinear.py:114-165
+    backward(dy, ctx, xi, rounding="rtn") -> (dx, dw)
+        qlinear.py:178-252
+
+same argument meaning, same ValueError cases, same seeds / stream tags, bit-identical quantizer
+outputs.  Tensors are CUDA torch tensors; every step runs in libquartet_b200.so:
+
+    forward : X_q, M_x = QuEST(H32(x));  W_q, M_w = QuEST(H32(w));  y = tcgen05(X_q, W_q)
+    dX      : G_q  = Q(H32(dy . s) * 3/4)          (qt_quant_bwd_rows)
+              Wt_q = Q(H32(deq(W_q)^T . s) * 3/4)  (qt_requant_t)
+              dx   = H32(tcgen05(G_q, Wt_q) . M_x) * 16/9   (fused epilogue)
+    dW      : Gt_q = Q(H32(dy^T . s) * 3/4)        (qt_quant_bwd_cols)
+              Xt_q = Q(H32(deq(X_q)^T . s) * 3/4)  (qt_requant_t)
+              dw   = H32(tcgen05(Gt_q, Xt_q) . M_w) * 16/9
+
+Only the reference's default GemmPolicy (single accumulation, quantized operands) runs on the GPU;
+its double / exact policies are CPU test modes and are served by the oracle, not here.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .mxfp4 import GROUP, MXOperand, derive_seed, gemm, quant_cols, quant_rows, sign_bits
+
+PRE_SCALE = 0.75                     # qlinear.py:36
+POST_SCALE = 16.0 / 9.0              # qlinear.py:37
+_POST_F32 = float(torch.tensor(16.0 / 9.0, dtype=torch.float32))  # dt(POST_SCALE), qlinear.py:210
+_TAG_FWD_X, _TAG_FWD_W = 11, 12      # qlinear.py:40
+_TAG_BWD_G1, _TAG_BWD_W, _TAG_BWD_G2, _TAG_BWD_X = 21, 22, 23, 24   # qlinear.py:41
+
+KINDS = ("rtn_absmax", "sr_absmax", "quest")
+
+
+@dataclass(frozen=True)
+class QuantScheme:
+    """quantizers.QuantScheme (quantizers.py:29-53)."""
+
+    kind: str
+    group_size: int = GROUP
+    clip_candidates: int = 64
+    clip_range: tuple = (1.0 / 16.0, 1.0)
+
+    def __post_init__(self):
+        if self.kind not in KINDS:
+            raise ValueError(f"unknown scheme kind {self.kind!r}")
+        lo, hi = self.clip_range
+        if not (0.0 < lo <= hi <= 1.0):
+            raise ValueError(f"invalid clip_range {self.clip_range}")
+        if self.clip_candidates < 2:
+            raise ValueError("clip_candidates must be >= 2")
+
+
+RTN_ABSMAX = QuantScheme("rtn_absmax")
+SR_ABSMAX = QuantScheme("sr_absmax")
+QUEST = QuantScheme("quest")
+
+
+@dataclass(frozen=True)
+class GemmPolicy:
+    """qlinear.GemmPolicy (qlinear.py:44-71)."""
+
+    accumulation: str = "single"
+    operand_path: str = "quantized"
+
+    def __post_init__(self):
+        if self.accumulation not in ("single", "double"):
+            raise ValueError(f"unknown accumulation {self.accumulation!r}")
+        if self.operand_path not in ("quantized", "exact"):
+            raise ValueError(f"unknown operand path {self.operand_path!r}")
+
+    @property
+    def exact(self) -> bool:
+        return self.operand_path == "exact"
+
+
+DEFAULT_POLICY = GemmPolicy()
+EXACT_POLICY = GemmPolicy(accumulation="double", operand_path="exact")
+
+
+@dataclass
+class LayerContext:
+    """qlinear.LayerContext (qlinear.py:74-87); masks live in the operands as bitmaps."""
+
+    x_q: MXOperand
+    w_q: MXOperand
+    scheme: QuantScheme
+    policy: GemmPolicy
+    hadamard: bool
+    batch: int
+    d_in: int
+    d_out: int
+
+    @property
+    def m_x(self) -> torch.Tensor:
+        return self.x_q.mask_bool()
+
+    @property
+    def m_w(self) -> torch.Tensor:
+        return self.w_q.mask_bool()
+
+
+def _check_policy(policy: GemmPolicy, scheme: QuantScheme) -> None:
+    if policy.exact or policy.accumulation != "single":
+        raise NotImplementedError(
+            "the B200 path implements the default policy (fp32 accumulation of MXFP4 operands); "
+            "double/exact policies are CPU test modes of the reference (see oracle/)")
+    if scheme.group_size != GROUP:
+        raise NotImplementedError("MXFP4 on tcgen05 uses 32-element scale groups")
+    if scheme.kind == "quest" and scheme.clip_range[0] != 1.0 / 16.0:
+        raise NotImplementedError("QuEST kernel is specialised for clip_range[0] = 1/16")
+
+
+def _err_flag(device) -> torch.Tensor:
+    return torch.zeros(1, dtype=torch.int32, device=device)
+
+
+def _raise_if_nonfinite(err: torch.Tensor | None) -> None:
+    if err is not None and int(err.item()) != 0:
+        raise ValueError("non-finite input")
+
+
+def quantize_operand(m: torch.Tensor, scheme: QuantScheme, hadamard: bool, seed: int | None = None,
+                     err: torch.Tensor | None = None) -> MXOperand:
+    """transform_last_axis + apply_scheme (qlinear.py:139-157) as one fused kernel."""
+    transform = _lib.QT_TRANSFORM_HADAMARD if hadamard else _lib.QT_TRANSFORM_NONE
+    if scheme.kind == "quest":
+        return quant_rows(m, transform, _lib.QT_ROUND_QUEST, want_mask=True, err=err)
+    if scheme.kind == "rtn_absmax":
+        op = quant_rows(m, transform, _lib.QT_ROUND_RTN, want_mask=True, err=err)
+    else:
+        op = quant_rows(m, transform, _lib.QT_ROUND_SR, sr_seed=seed, want_mask=True, err=err)
+    return op
+
+
+def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, policy: GemmPolicy = DEFAULT_POLICY,
+            hadamard: bool = True, seed: int | None = None, out_dtype: torch.dtype = torch.float32,
+            check_finite: bool = True):
+    """y = x @ w.T through the quantized pipeline; returns (y, context)  (qlinear.py:114-165)."""
+    _check_policy(policy, scheme)
+    if x.dim() != 2 or w.dim() != 2:
+        raise ValueError("x and w must be 2-D")
+    batch, d_in = x.shape
+    d_out, d_in_w = w.shape
+    if d_in != d_in_w:
+        raise ValueError(f"shape mismatch: x has {d_in} features, w has {d_in_w}")
+    g = scheme.group_size
+    if d_in % g != 0:
+        raise ValueError(f"input dimension {d_in} not divisible by block size {g}")
+    sx = sw = None
+    if scheme.kind == "sr_absmax":
+        if seed is None:
+            raise ValueError("sr_absmax forward requires a seed")
+        sx = derive_seed(seed, _TAG_FWD_X)
+        sw = derive_seed(seed, _TAG_FWD_W)
+    err = _err_flag(x.device) if check_finite else None
+    x_q = quantize_operand(x, scheme, hadamard, sx, err)
+    w_q = quantize_operand(w, scheme, hadamard, sw, err)
+    y = gemm(x_q, w_q, out_dtype=out_dtype)
+    _raise_if_nonfinite(err)
+    ctx = LayerContext(x_q=x_q, w_q=w_q, scheme=scheme, policy=policy, hadamard=hadamard,
+                       batch=batch, d_in=d_in, d_out=d_out)
+    return y, ctx
+
+
+def _rounding_code(rounding: str) -> int:
+    if rounding == "rtn":
+        return _lib.QT_ROUND_RTN
+    if rounding == "sr":
+        return _lib.QT_ROUND_SR
+    if rounding == "exact":
+        raise NotImplementedError("rounding='exact' skips quantization: a CPU test mode (oracle), not a GPU path")
+    raise ValueError(f"unknown backward rounding {rounding!r}")
+
+
+def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn",
+             dx_dtype: torch.dtype = torch.float32, dw_dtype: torch.dtype = torch.float32,
+             check_finite: bool = True, return_operands: bool = False):
+    """Input and weight gradients from the saved context and upstream dy (qlinear.py:178-252)."""
+    if rounding not in ("exact", "rtn", "sr"):
+        raise ValueError(f"unknown backward rounding {rounding!r}")
+    rc = _rounding_code(rounding)
+    if tuple(dy.shape) != (ctx.batch, ctx.d_out):
+        raise ValueError(f"dy shape {tuple(dy.shape)}, expected {(ctx.batch, ctx.d_out)}")
+    g = ctx.scheme.group_size
+    if ctx.d_out % g != 0:
+        raise ValueError(f"output dimension {ctx.d_out} not divisible by block size {g}")
+    if ctx.batch % g != 0:
+        raise ValueError(f"batch size {ctx.batch} not divisible by block size {g}")
+    dev = dy.device
+    transform = _lib.QT_TRANSFORM_RANDOMIZED if ctx.hadamard else _lib.QT_TRANSFORM_NONE
+    signs = sign_bits(xi, max(ctx.batch, ctx.d_out), dev) if ctx.hadamard else None
+    sr = rounding == "sr"
+    err = _err_flag(dev) if check_finite else None
+
+    # input gradient: contract over d_out (qlinear.py:212-230)
+    g_q = quant_rows(dy, transform, rc, signs=signs, prescale=PRE_SCALE,
+                     sr_seed=derive_seed(xi, _TAG_BWD_G1) if sr else 0, err=err)
+    wt_q = quant_cols(ctx.w_q, rc, transform=transform, signs=signs, prescale=PRE_SCALE,
+                      sr_seed=derive_seed(xi, _TAG_BWD_W) if sr else 0, err=err)
+    dx = gemm(g_q, wt_q, out_dtype=dx_dtype, mask=ctx.x_q.mask, hadamard=ctx.hadamard, scale=_POST_F32)
+
+    # weight gradient: contract over batch (qlinear.py:232-250)
+    gt_q = quant_cols(dy, rc, transform=transform, signs=signs, prescale=PRE_SCALE,
+                      sr_seed=derive_seed(xi, _TAG_BWD_G2) if sr else 0, err=err)
+    xt_q = quant_cols(ctx.x_q, rc, transform=transform, signs=signs, prescale=PRE_SCALE,
+                      sr_seed=derive_seed(xi, _TAG_BWD_X) if sr else 0, err=err)
+    dw = gemm(gt_q, xt_q, out_dtype=dw_dtype, mask=ctx.w_q.mask, hadamard=ctx.hadamard, scale=_POST_F32)
+    _raise_if_nonfinite(err)
+    if return_operands:
+        return dx, dw, {"g_q": g_q, "wt_q": wt_q, "gt_q": gt_q, "xt_q": xt_q}
+    return dx, dw

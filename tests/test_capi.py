@@ -1,0 +1,61 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol include/*.h declares, and
+its host-only helpers agree with the oracle.  No compute kernels are launched (no GPU here)."""
+
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2505_14669_b200 import _lib
+    from paper_2505_14669_b200.build import build
+
+    build()
+    return _lib.load()
+
+
+def _declared():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        names |= set(re.findall(r"QT_API\s+[\w\s\*]+?\b(qt_\w+)\s*\(", open(h).read()))
+    return names
+
+
+def test_header_declares_entry_points():
+    names = _declared()
+    for must in ("qt_quant_fwd_quest", "qt_quant_bwd_rows", "qt_quant_bwd_cols", "qt_requant_t", "qt_gemm_mxf4",
+                 "qt_quant_rows", "qt_quant_cols", "qt_sign_bits"):
+        assert must in names
+
+
+def test_every_declared_symbol_exported(lib):
+    from paper_2505_14669_b200._lib import SIGNATURES
+
+    for name in _declared():
+        assert hasattr(lib, name), name
+        assert name in SIGNATURES, f"{name} has no ctypes signature"
+
+
+def test_host_helpers(lib, oracle):
+    assert lib.qt_abi_version() == 1
+    assert lib.qt_error_string(2001).decode().startswith("shape")
+    assert lib.qt_codes_ld(1024) == 512
+    assert lib.qt_sf_katoms(640) == 6
+    assert lib.qt_sf_bytes(300, 1024) == 2 * 2 * 8 * 512
+    arr = (ctypes.c_uint64 * 2)(7, 21)
+    assert lib.qt_derive_seed(ctypes.cast(arr, ctypes.c_void_p), 2) == oracle.derive_seed(7, 21)
+    assert lib.qt_mix64(12345) == oracle.mix64(12345)
+
+
+def test_argument_errors_without_gpu(lib):
+    # shape / enum validation happens before any CUDA call
+    assert lib.qt_quant_rows(None, 0, 33, 4, 33, 0, None, 1.0, 0, 0, 0, None, 16, None, 2, None, None, None,
+                             None) == 2001
+    assert lib.qt_gemm_mxf4(None, None, None, None, 32, 32, 48, None, 0, 32, 0, None, 1.0, None) == 2001
+    assert lib.qt_gemm_mxf4(None, None, None, None, 32, 32, 64, None, 7, 32, 0, None, 1.0, None) == 2003

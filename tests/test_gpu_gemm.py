@@ -1,0 +1,103 @@
+"""tcgen05 MXFP4 GEMM vs the reference's dequantize-then-matmul (gemm_lp, qlinear.py:96-111).
+
+Tolerance (stated): the GPU accumulates the exact FP4 x FP4 x E8M0 products in fp32 in a different
+order than the reference's sequential fp32 loop, so results are compared with a relative Frobenius
+error against the float64 product of the dequantized operands:
+    err(GPU) <= max(4 * err(reference fp32 loop), 1e-6).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from gpu_util import bf16_values, rel_err, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def qt():
+    import paper_2505_14669_b200 as qt
+
+    qt.load()
+    return qt
+
+
+def _operand(qt, x: np.ndarray):
+    return qt.quant_rows(to_dev(x), qt._lib.QT_TRANSFORM_NONE, qt._lib.QT_ROUND_RTN)
+
+
+def _check(qt, oracle, a, b, out_dtype=torch.float32):
+    A, B = _operand(qt, a), _operand(qt, b)
+    got = qt.gemm(A, B, out_dtype=out_dtype).float().cpu().numpy()
+    ac, as_ = oracle.quantize_rtn(a.astype(np.float64), 32)
+    bc, bs = oracle.quantize_rtn(b.astype(np.float64), 32)
+    ad, bd = oracle.dequantize(ac, as_, 32), oracle.dequantize(bc, bs, 32)
+    exact = ad @ bd.T
+    ref32 = oracle.gemm_nt(ad.astype(np.float32), bd.astype(np.float32))
+    e_gpu, e_ref = rel_err(got, exact), rel_err(ref32, exact)
+    tol = max(4 * e_ref, 1e-6) if out_dtype == torch.float32 else 4e-3
+    assert e_gpu <= tol, (e_gpu, e_ref, a.shape, b.shape)
+    return e_gpu, e_ref
+
+
+def test_gemm_identity_like(qt):
+    """test_qlinear.py:146-149: quantize(6 I) squared is 36 I exactly."""
+    q6 = qt.quant_rows(torch.eye(32, device="cuda") * 6.0, qt._lib.QT_TRANSFORM_NONE, qt._lib.QT_ROUND_RTN)
+    out = qt.gemm(q6, q6).cpu().numpy()
+    assert np.array_equal(out, 36.0 * np.eye(32))
+
+
+def test_gemm_structured_scales(qt):
+    """Per-row / per-column / per-group scales land in the right place (SF layout check)."""
+    M, N, K = 256, 256, 512
+    a = np.zeros((M, K), np.float32)
+    b = np.zeros((N, K), np.float32)
+    r = np.random.default_rng(0)
+    # group-constant powers of two: exact in MXFP4, every partial sum exact in fp32 (< 2^17 span)
+    a[:] = np.ldexp(1.0, (np.arange(M)[:, None] % 3) - 1 + (np.arange(K)[None, :] // 32) % 2)
+    b[:] = np.ldexp(1.0, (np.arange(N)[:, None] % 3) - 1 + (np.arange(K)[None, :] // 32) % 3)
+    a *= r.choice([-1.0, 1.0], size=a.shape)
+    b *= r.choice([-1.0, 1.0], size=b.shape)
+    A, B = _operand(qt, a), _operand(qt, b)
+    got = qt.gemm(A, B).cpu().numpy()
+    exact = a.astype(np.float64) @ b.astype(np.float64).T   # powers of two are exact in MXFP4
+    assert np.array_equal(got, exact)
+
+
+@pytest.mark.parametrize("mnk", [(128, 256, 256), (256, 512, 1024), (2048, 1024, 1024), (96, 160, 640),
+                                 (300, 96, 96), (1024, 1152, 2048)])
+def test_gemm_random(qt, oracle, mnk):
+    M, N, K = mnk
+    r = np.random.default_rng(M + N + K)
+    a = bf16_values(r.normal(size=(M, K)).astype(np.float32))
+    b = bf16_values(r.standard_t(df=3, size=(N, K)).astype(np.float32))
+    e_gpu, e_ref = _check(qt, oracle, a, b)
+    print(f"gemm {mnk}: rel err gpu {e_gpu:.3e} ref-fp32 {e_ref:.3e}")
+
+
+def test_gemm_bf16_out(qt, oracle):
+    r = np.random.default_rng(3)
+    _check(qt, oracle, r.normal(size=(256, 512)).astype(np.float32), r.normal(size=(256, 512)).astype(np.float32),
+           out_dtype=torch.bfloat16)
+
+
+def test_gemm_mask_hadamard_epilogue(qt, oracle):
+    """dx = FWHT(dx_q * m) * fp32(16/9) fused in the epilogue (qlinear.py:229-230)."""
+    M, N, K = 256, 512, 256
+    r = np.random.default_rng(4)
+    a = r.normal(size=(M, K)).astype(np.float32)
+    b = r.normal(size=(N, K)).astype(np.float32)
+    A, B = _operand(qt, a), _operand(qt, b)
+    m = r.random((M, N)) < 0.9
+    words = np.zeros((M, N // 32), np.uint32)
+    for j in range(32):
+        words |= m[:, j::32].astype(np.uint32) << j
+    mask = torch.from_numpy(words.view(np.int32)).cuda()
+    post = np.float32(16.0 / 9.0)
+    got = qt.gemm(A, B, mask=mask, scale=float(post)).cpu().numpy()
+    plain = qt.gemm(A, B).cpu().numpy()
+    ref = oracle.fwht((plain * m).astype(np.float32), 32) * post
+    assert np.array_equal(got, ref)   # same fp32 accumulator -> epilogue must be bit-exact
+    got_nh = qt.gemm(A, B, mask=mask, hadamard=False, scale=float(post)).cpu().numpy()
+    assert np.array_equal(got_nh, (plain * m).astype(np.float32) * post)

@@ -1,0 +1,194 @@
+"""GPU quantizers vs the CPU oracle: bit-exact FP4 codes, E8M0 scales and trust masks.
+
+The oracle (oracle/, pinned to the reference by test_oracle_golden.py) restates
+mx4train/_backend/_native.pyx; the GPU kernels are called through the C ABI
+(libquartet_b200.so) via paper_2505_14669_b200.mxfp4.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from gpu_util import assert_operand_equal, bf16_values, op_codes, op_scales, to_dev
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def qt():
+    import paper_2505_14669_b200 as qt
+
+    qt.load()
+    return qt
+
+
+def _fp32_inputs():
+    z = np.load(os.path.join(GOLDEN, "kernels.npz"))
+    out = []
+    for i in range(int(z["n"])):
+        x = z[f"x{i}"]
+        if x.shape[1] % 32:
+            x = x[:, : (x.shape[1] // 32) * 32]
+        if x.shape[1] == 0:
+            continue
+        out.append((i, x.astype(np.float32)))
+    return out
+
+
+def _edge_matrix():
+    """Grid midpoints, exact grid points, signed zeros, huge/tiny ranges, +-6 saturation."""
+    r = np.random.default_rng(5)
+    rows = []
+    mids = np.array([0.25, 0.75, 1.25, 1.75, 2.5, 3.5, 5.0, 6.0, 7.0, 0.0, -0.0, 0.5, 1.0, 1.5, 2.0, 3.0])
+    for s in (1.0, 2.0**-3, 2.0**7, 2.0**-120, 2.0**100):
+        rows.append(np.concatenate([mids, -mids]) * s)
+        rows.append(np.concatenate([np.nextafter(mids, 10), np.nextafter(mids, -10)]) * s)
+    rows.append(np.ldexp(1.0, np.arange(-60, 4, 2)))
+    rows.append(r.standard_t(df=1.2, size=32) * 1e3)
+    rows.append(np.full(32, 1.5 * 2.0**-3))
+    rows.append(np.zeros(32))
+    m = np.stack(rows).astype(np.float32)
+    return m
+
+
+@pytest.mark.parametrize("rounding", ["quest", "rtn", "sr"])
+def test_quantizers_golden_inputs(qt, oracle, rounding):
+    L = qt._lib
+    inputs = _fp32_inputs() + [("edge", _edge_matrix())]
+    for i, x in inputs:
+        xd = to_dev(x)
+        if rounding == "quest":
+            op = qt.quant_rows(xd, L.QT_TRANSFORM_NONE, L.QT_ROUND_QUEST, want_mask=True)
+            c, s, m = oracle.quantize_quest(x.astype(np.float64), 32, 1.0 / 16.0)
+            assert np.array_equal(op.mask_bool().cpu().numpy(), m.astype(bool)), i
+        elif rounding == "rtn":
+            op = qt.quant_rows(xd, L.QT_TRANSFORM_NONE, L.QT_ROUND_RTN)
+            c, s = oracle.quantize_rtn(x.astype(np.float64), 32)
+        else:
+            op = qt.quant_rows(xd, L.QT_TRANSFORM_NONE, L.QT_ROUND_SR, sr_seed=1234, counter_start=17)
+            c, s = oracle.quantize_sr(x.astype(np.float64), 32, 1234, 17)
+        assert_operand_equal(op, c, s, f"{rounding} input {i}")
+
+
+def test_packed_bytes_equal_reference_layout(qt, oracle):
+    """codes bytes == reference pack_nibbles(codes) (element 2k in the low nibble)."""
+    L = qt._lib
+    x = bf16_values(np.random.default_rng(0).normal(size=(64, 256)).astype(np.float32))
+    op = qt.quant_rows(to_dev(x), L.QT_TRANSFORM_NONE, L.QT_ROUND_RTN)
+    c, _ = oracle.quantize_rtn(x.astype(np.float64), 32)
+    assert np.array_equal(op.codes.cpu().numpy(), oracle.pack_nibbles(c))
+
+
+@pytest.mark.parametrize("shape", [(2048, 1024), (96, 640), (32, 32)])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_forward_quantizer_h32_quest(qt, oracle, shape, dtype):
+    """x_h = FWHT32(x) (fp32 butterfly), QuEST: qlinear.py:139-141, 156."""
+    r = np.random.default_rng(shape[0] + shape[1])
+    x = r.standard_t(df=4, size=shape).astype(np.float32)
+    if dtype == torch.bfloat16:
+        x = bf16_values(x)
+    xd = to_dev(x, dtype)
+    fb = torch.zeros(1, dtype=torch.int32, device="cuda")
+    op = qt.quant_rows(xd, qt._lib.QT_TRANSFORM_HADAMARD, qt._lib.QT_ROUND_QUEST, want_mask=True, fallbacks=fb)
+    xh = oracle.fwht(x, 32)
+    c, s, m = oracle.quantize_quest(xh.astype(np.float64), 32, 1.0 / 16.0)
+    assert_operand_equal(op, c, s, "fwd quest")
+    assert np.array_equal(op.mask_bool().cpu().numpy(), m.astype(bool))
+    print("quest exact-search fallbacks:", int(fb.item()), "of", shape[0] * shape[1] // 32)
+
+
+@pytest.mark.parametrize("rounding", ["rtn", "sr"])
+def test_backward_row_quantizer(qt, oracle, rounding):
+    """G_q = Q(FWHT(dy * s_xi) * 0.75) (qlinear.py:214, 219, 225)."""
+    T, d_out, xi = 256, 384, 7
+    dy = bf16_values(np.random.default_rng(1).normal(size=(T, d_out)).astype(np.float32))
+    signs = qt.sign_bits(xi, max(T, d_out), "cuda")
+    rc = qt._lib.QT_ROUND_RTN if rounding == "rtn" else qt._lib.QT_ROUND_SR
+    seed = oracle.derive_seed(xi, 21)
+    op = qt.quant_rows(to_dev(dy, torch.bfloat16), qt._lib.QT_TRANSFORM_RANDOMIZED, rc, signs=signs, prescale=0.75,
+                       sr_seed=seed)
+    gh = oracle.fwht(dy * oracle.signs(xi, 0, d_out), 32) * np.float32(0.75)
+    if rounding == "rtn":
+        c, s = oracle.quantize_rtn(gh.astype(np.float64), 32)
+    else:
+        c, s = oracle.quantize_sr(gh.astype(np.float64), 32, seed, 0)
+    assert_operand_equal(op, c, s, "bwd rows")
+
+
+@pytest.mark.parametrize("rounding", ["rtn", "sr"])
+@pytest.mark.parametrize("shape", [(256, 384), (160, 96)])
+def test_backward_col_quantizer(qt, oracle, rounding, shape):
+    """Gt_q = Q(FWHT(dy^T * s_xi) * 0.75) (qlinear.py:234, 239, 245)."""
+    T, d_out = shape
+    xi = 9
+    dy = bf16_values(np.random.default_rng(2).normal(size=(T, d_out)).astype(np.float32))
+    signs = qt.sign_bits(xi, max(T, d_out), "cuda")
+    rc = qt._lib.QT_ROUND_RTN if rounding == "rtn" else qt._lib.QT_ROUND_SR
+    seed = oracle.derive_seed(xi, 23)
+    op = qt.quant_cols(to_dev(dy, torch.bfloat16), rc, transform=qt._lib.QT_TRANSFORM_RANDOMIZED, signs=signs,
+                       prescale=0.75, sr_seed=seed)
+    gt = oracle.fwht(np.ascontiguousarray(dy.T) * oracle.signs(xi, 0, T), 32) * np.float32(0.75)
+    if rounding == "rtn":
+        c, s = oracle.quantize_rtn(gt.astype(np.float64), 32)
+    else:
+        c, s = oracle.quantize_sr(gt.astype(np.float64), 32, seed, 0)
+    assert_operand_equal(op, c, s, "bwd cols")
+
+
+@pytest.mark.parametrize("rounding", ["rtn", "sr"])
+def test_requant_transpose(qt, oracle, rounding):
+    """Xt_q = Q(FWHT(deq(X_q)^T * s_xi) * 0.75) (qlinear.py:207, 235, 240, 246)."""
+    T, d_in, xi = 384, 256, 11
+    x = bf16_values(np.random.default_rng(3).normal(size=(T, d_in)).astype(np.float32))
+    xq = qt.quant_rows(to_dev(x, torch.bfloat16), qt._lib.QT_TRANSFORM_HADAMARD, qt._lib.QT_ROUND_QUEST,
+                       want_mask=True)
+    signs = qt.sign_bits(xi, T, "cuda")
+    rc = qt._lib.QT_ROUND_RTN if rounding == "rtn" else qt._lib.QT_ROUND_SR
+    seed = oracle.derive_seed(xi, 24)
+    op = qt.quant_cols(xq, rc, transform=qt._lib.QT_TRANSFORM_RANDOMIZED, signs=signs, prescale=0.75, sr_seed=seed)
+    xc, xs, _ = oracle.quantize_quest(oracle.fwht(x, 32).astype(np.float64), 32, 1.0 / 16.0)
+    xval = oracle.dequantize(xc, xs, 32, np.float32)
+    xt = oracle.fwht(np.ascontiguousarray(xval.T) * oracle.signs(xi, 0, T), 32) * np.float32(0.75)
+    if rounding == "rtn":
+        c, s = oracle.quantize_rtn(xt.astype(np.float64), 32)
+    else:
+        c, s = oracle.quantize_sr(xt.astype(np.float64), 32, seed, 0)
+    assert_operand_equal(op, c, s, "requant-transpose")
+
+
+def test_sign_bits_match_rng(qt, oracle):
+    for xi, n in ((7, 4096), (2**64 - 1, 333), (0, 32)):
+        bits = qt.sign_bits(xi, n, "cuda").cpu().numpy().view(np.uint32)
+        flips = ((bits[np.arange(n) // 32] >> (np.arange(n) % 32)) & 1).astype(bool)
+        assert np.array_equal(flips, oracle.signs(xi, 0, n) < 0)
+
+
+def test_derive_seed_matches(qt, oracle):
+    for parts in ((7, 21), (2**64 - 1, 24), (3, 4, 5)):
+        assert qt.derive_seed(*parts) == oracle.derive_seed(*parts)
+
+
+def test_nonfinite_flag(qt):
+    x = torch.zeros(32, 64, device="cuda")
+    x[3, 5] = float("nan")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    qt.quant_rows(x, qt._lib.QT_TRANSFORM_HADAMARD, qt._lib.QT_ROUND_QUEST, want_mask=True, err=err)
+    assert int(err.item()) == 1
+    with pytest.raises(ValueError):
+        qt.forward(x, torch.ones(32, 64, device="cuda"))
+
+
+def test_sr_unbiased_known_answer(qt):
+    """test_quantizers.py:43-56: 2.4 at scale 1 rounds to 3 with P = 0.4."""
+    n = 200_000
+    x = torch.zeros(n, 32, device="cuda")
+    x[:, 0] = 6.0
+    x[:, 1] = 2.4
+    op = qt.quant_rows(x, qt._lib.QT_TRANSFORM_NONE, qt._lib.QT_ROUND_SR, sr_seed=5)
+    vals = op.dequantize(torch.float64)[:, 1].cpu().numpy()
+    assert set(np.unique(vals)) <= {2.0, 3.0}
+    assert abs((vals == 3.0).mean() - 0.4) < 0.005
