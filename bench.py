@@ -1,0 +1,408 @@
+"""Benchmark: QuartetLinear fwd+bwd at Llama-7B shapes (BASELINE.json configs[2]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--tokens T]
+
+One step = forward + backward of the Quartet linear layer (Alg. 1) for each of the three Llama-7B
+projection shapes (4096->4096, 4096->11008, 11008->4096) on T tokens per GPU, through the
+reference-mirroring functional API (paper_2505_14669_b200.forward / backward -> C ABI -> sm_100a
+kernels).  Inputs are synthetic and resident in HBM; every input tensor is larger than L2 (126 MB
+for x / dy at T=16384), so no L2 flush is needed between steps.
+
+Multi-GPU (torchrun): data-parallel, weak scaling; each rank runs its own T tokens and the dW of
+every shape is all-reduced in bf16 over NCCL (the only exchange step in DP training).
+
+--impl reference times the reference algorithm on the host CPU (oracle/ C restatement of
+mx4train's native kernels, all host threads) on a bounded token slice of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QuartetLinear fwd+bwd TFLOPS vs BF16 (Llama-7B shapes); train tok/s @1–8 GPU"
+SHAPES = [(4096, 4096), (4096, 11008), (11008, 4096)]   # (d_in, d_out)
+
+
+def flops_per_step(tokens: int) -> float:
+    return float(sum(6 * tokens * di * do for di, do in SHAPES))
+
+
+# --------------------------------------------------------------------------- clocks sampler
+class ClockSampler:
+    """Samples SM clocks and throttle reasons through NVML (in-process, no nvidia-smi fork) every
+    `period` seconds from a background thread while the timed region runs."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index: int, period: float = 0.02):
+        self.index, self.period = index, period
+        self.samples = []
+        self._stop = threading.Event()
+        self._thread = None
+        self.smax = None
+
+    def start(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+            return
+        self._thread = threading.Thread(target=self._run, daemon=True)
+        self._thread.start()
+
+    def _run(self):
+        nv, h = self._nv, self._h
+        while not self._stop.is_set():
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                     nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def stop(self) -> dict:
+        if self._thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self._stop.set()
+        self._thread.join()
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        sm = [c for c, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax, "reasons": reasons,
+                "samples": len(sm), "source": "NVML nvmlDeviceGetClockInfo / CurrentClocksEventReasons"}
+
+
+# ------------------------------------------------------------------------------ helpers
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"], "source": "MEASURED_PEAKS.json"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def ncu_traffic() -> dict:
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+def cpu_baseline_sample(threads: int, tokens: int = 256) -> dict:
+    """The reference algorithm on the host (oracle port), one fwd+bwd per shape on a token slice."""
+    import numpy as np
+
+    from oracle import oracle
+
+    oracle.build()
+    oracle.set_threads(threads)
+    r = np.random.default_rng(0)
+    total_flop, total_s = 0.0, 0.0
+    for d_in, d_out in SHAPES:
+        x = r.standard_normal((tokens, d_in), dtype=np.float32)
+        w = (r.standard_normal((d_out, d_in), dtype=np.float32) / np.sqrt(d_in)).astype(np.float32)
+        dy = r.standard_normal((tokens, d_out), dtype=np.float32)
+        t0 = time.perf_counter()
+        _, ctx = oracle.forward(x, w)
+        oracle.backward(dy, ctx, xi=7)
+        total_s += time.perf_counter() - t0
+        total_flop += 6.0 * tokens * d_in * d_out
+    oracle.set_threads(1)
+    return {"flop": total_flop, "seconds": total_s}
+
+
+# ---------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_14669_b200 as qt
+    from paper_2505_14669_b200 import mxfp4
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    qt.load()
+    T = args.tokens
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    data = []
+    for d_in, d_out in SHAPES:
+        x = torch.randn(T, d_in, device=dev, generator=g).to(torch.bfloat16)
+        w = torch.randn(d_out, d_in, device=dev, generator=g) / (d_in ** 0.5)
+        dy = torch.randn(T, d_out, device=dev, generator=g).to(torch.bfloat16)
+        data.append((x, w, dy))
+
+    gemm_events = []   # (start, end) pairs recorded around every GEMM launch in the timed region
+    quant_events = []
+    record = {"on": False}
+    orig_gemm, orig_rows, orig_cols = mxfp4.gemm, mxfp4.quant_rows, mxfp4.quant_cols
+
+    def timed(fn, store):
+        def wrapper(*a, **k):
+            if not record["on"]:
+                return fn(*a, **k)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            out = fn(*a, **k)
+            e.record()
+            store.append((s, e, a, k))
+            return out
+        return wrapper
+
+    import paper_2505_14669_b200.qlinear as ql
+    ql.gemm = timed(orig_gemm, gemm_events)
+    ql.quant_rows = timed(orig_rows, quant_events)
+    ql.quant_cols = timed(orig_cols, quant_events)
+    launches = {"n": 0}
+    counted = {}
+
+    def step(xi):
+        for i, (x, w, dy) in enumerate(data):
+            y, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False)
+            dx, dw = qt.backward(dy, ctx, xi=xi * 3 + i, dx_dtype=torch.bfloat16, dw_dtype=torch.float32,
+                                 check_finite=False)
+            if world > 1:
+                dwb = dw.to(torch.bfloat16)
+                dist.all_reduce(dwb)
+        return
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local_rank) if rank == 0 and not args.no_clocks else None
+    if sampler:
+        sampler.start()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    record["on"] = True
+    start.record()
+    for i in range(args.steps):
+        step(args.warmup + i)
+    end.record()
+    torch.cuda.synchronize()
+    record["on"] = False
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop() if sampler else None
+    ms = start.elapsed_time(end) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ql.gemm, ql.quant_rows, ql.quant_cols = orig_gemm, orig_rows, orig_cols
+
+    # per-launch kernel times (CUDA events on the launching stream, timed region only)
+    gemm_ms = sum(s.elapsed_time(e) for s, e, _, _ in gemm_events)
+    gemm_flop = sum(2.0 * a[0].rows * a[1].rows * a[0].cols for _, _, a, _ in gemm_events)
+    quant_ms = sum(s.elapsed_time(e) for s, e, _, _ in quant_events)
+
+    def quant_bytes(a, k):
+        src = a[0]
+        if hasattr(src, "codes"):   # MXFP4 operand in -> requant-transpose
+            n = src.rows * src.cols
+            return n * (0.5 + 1 / 32) * 2
+        n = src.numel()
+        out = n * (0.5 + 1 / 32) + (n / 8 if k.get("want_mask") else 0)
+        return n * src.element_size() + out
+    qbytes = sum(quant_bytes(a, k) for _, _, a, k in quant_events)
+    # our kernels in the timed region: every quantizer + GEMM launch, plus one sign-bitmap kernel per backward
+    gpu_launches = len(gemm_events) + len(quant_events) + len(SHAPES) * args.steps
+
+    # bf16 cuBLAS comparator on the same shapes (3 GEMMs per shape: y, dx, dw)
+    bf16_ms = None
+    if rank == 0:
+        mats = []
+        for (x, w, dy) in data:
+            mats.append((x, w.to(torch.bfloat16), dy))
+
+        def bf16_step():
+            for x, wb, dy in mats:
+                torch.matmul(x, wb.t())
+                torch.matmul(dy, wb)
+                torch.matmul(dy.t(), x)
+        for _ in range(3):
+            bf16_step()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.steps):
+            bf16_step()
+        e.record()
+        torch.cuda.synchronize()
+        bf16_ms = s.elapsed_time(e) / args.steps
+
+    # end-to-end through the public API with host buffers (H2D inputs, D2H results)
+    e2e = None
+    if rank == 0:
+        host = [(x.cpu().pin_memory(), dy.cpu().pin_memory()) for (x, _, dy) in data]
+        outs = [(torch.empty(x.shape, dtype=torch.bfloat16).pin_memory(),
+                 torch.empty(w.shape, dtype=torch.float32).pin_memory()) for (x, w, _) in data]
+
+        def e2e_step(xi):
+            h2d = d2h = 0
+            for i, ((hx, hdy), (w_dev), (ox, ow)) in enumerate(zip(host, [d[1] for d in data], outs)):
+                xd = hx.to(dev, non_blocking=True)
+                dyd = hdy.to(dev, non_blocking=True)
+                h2d += hx.numel() * 2 + hdy.numel() * 2
+                y, ctx = qt.forward(xd, w_dev, out_dtype=torch.bfloat16, check_finite=False)
+                dx, dw = qt.backward(dyd, ctx, xi=xi * 3 + i, dx_dtype=torch.bfloat16, check_finite=False)
+                ox.copy_(dx, non_blocking=True)
+                ow.copy_(dw, non_blocking=True)
+                d2h += dx.numel() * 2 + dw.numel() * 4
+            return h2d, d2h
+        for i in range(2):
+            e2e_step(i)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for i in range(args.steps):
+            h2d, d2h = e2e_step(100 + i)
+        e.record()
+        torch.cuda.synchronize()
+        e2e_ms = s.elapsed_time(e) / args.steps
+        e2e = {"value": flops_per_step(T) / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "paper_2505_14669_b200.forward/backward (C ABI) with pinned host x/dy in, dx/dw out"}
+
+    if rank != 0:
+        return None
+    peaks = measured_peaks()
+    fp4_peak = 4.0 * peaks["bf16_tflops"]
+    gemm_tflops = gemm_flop / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None
+    traffic = ncu_traffic().get("gemm_dram_bytes_per_launch")
+    avg_flop = gemm_flop / max(1, len(gemm_events))
+    value = world * flops_per_step(T) / (ms * 1e-3) / 1e12
+    out = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "mxfp4-e2m1 x e2m1 (E8M0 block-32 scales), fp32 accumulate",
+        "data": "synthetic (x, dy ~ N(0,1) bf16; W ~ N(0,1/d_in) fp32 master)",
+        "config": {"workload": "QuartetLinear fwd+bwd, Llama-7B projection shapes (BASELINE configs[2])",
+                   "shapes_din_dout": SHAPES, "tokens_per_gpu": T, "global_tokens": T * world,
+                   "scheme": "quest fwd / rtn bwd, hadamard g=32", "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (x/dy 128-344 MB per shape); no flush needed"},
+        "tokens_per_s": round(world * T * len(SHAPES) / (ms * 1e-3), 1),
+        "bf16_cublas": None if bf16_ms is None else {
+            "value": round(flops_per_step(T) / (bf16_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+            "ms_per_step": round(bf16_ms, 4), "speedup_ours": round(bf16_ms / (ms), 3),
+            "what": "torch.matmul bf16: y = x W^T, dx = dy W, dw = dy^T x per shape"},
+        "roofline": {"kernel": "k_gemm_mxf4 (tcgen05 kind::mxf4)", "bound": "tensor",
+                     "achieved": round(gemm_tflops, 1) if gemm_tflops else None,
+                     "peak": round(fp4_peak, 1), "unit": "TFLOP/s",
+                     "frac": round(gemm_tflops / fp4_peak, 4) if gemm_tflops else None,
+                     "traffic": traffic,
+                     "peak_source": f"4 x bf16_tflops of {peaks['source']} (dense FP4 = 4x dense BF16); "
+                                    "spec 9000 TFLOP/s",
+                     "flop_per_launch_avg": avg_flop, "launches": len(gemm_events),
+                     "share_of_step": round(gemm_ms / args.steps / ms, 4)},
+        "quantizer_roofline": {"bound": "hbm", "achieved": round(qbytes / (quant_ms * 1e-3) / 1e9, 1) if quant_ms
+                               else None, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                               "frac": round(qbytes / (quant_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4)
+                               if quant_ms else None,
+                               "share_of_step": round(quant_ms / args.steps / ms, 4)},
+        "e2e": e2e,
+        "gpu_launches": gpu_launches,
+        "clocks": clocks,
+    }
+    return out
+
+
+def run_reference(args, rank, world):
+    """Reference CPU implementation (oracle port of mx4train's native kernels), all host threads."""
+    if rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    sample_tokens = args.ref_tokens
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        cpu_baseline_sample(threads, sample_tokens)
+    vals = []
+    t_all = 0.0
+    for _ in range(args.steps):
+        r = cpu_baseline_sample(threads, sample_tokens)
+        vals.append(r["flop"] / r["seconds"] / 1e12)
+        t_all += r["seconds"]
+    v = statistics.median(vals)
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t_all / args.steps, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (simulated MXFP4)",
+        "data": "synthetic", "config": {"workload": "QuartetLinear fwd+bwd, Llama-7B projection shapes",
+                                        "shapes_din_dout": SHAPES, "tokens_per_step": sample_tokens},
+        "cpu_baseline": {"value": round(v, 5), "unit": "TFLOP/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample_tokens} tokens x 3 shapes per step (bounded slice of 16384)"},
+        "e2e": {"value": round(v, 5), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tokens", type=int, default=16384)
+    ap.add_argument("--ref-tokens", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+
+    import torch.distributed as dist
+
+    if world > 1:
+        import torch
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_ours(args, rank, world, local_rank)
+    if out is not None and world == 1 and not args.no_cpu_baseline:
+        r = cpu_baseline_sample(1, 128)
+        out["cpu_baseline"] = {"value": round(r["flop"] / r["seconds"] / 1e12, 6), "unit": "TFLOP/s", "cores": 1,
+                               "kind": "port", "sample": "128 tokens x 3 shapes, one fwd+bwd each (oracle/, "
+                                                          "single-threaded like the reference's Cython kernels)",
+                               "seconds": round(r["seconds"], 2)}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

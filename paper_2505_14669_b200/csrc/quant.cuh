@@ -27,18 +27,17 @@ __device__ __forceinline__ double grid_round_d(double a) {
 
 // Exact reference scale search (_native.pyx:171-203) -- cold path for near-ties of the fast
 // search.  Sequential ascending-j f64 accumulation, strict '<' (ties keep the larger scale).
-__device__ __noinline__ int quest_exact(const float* x, int e_hi, int e_lo) {
-    double vb[32];
-    double inv = (double)exp2i(127 - e_hi);  // 1 / s_hi, exact
-#pragma unroll
-    for (int j = 0; j < 32; ++j) vb[j] = (double)x[j] * inv;
+// vbuf[j] * 2^k of the reference equals |x_j| * 2^(127-e) exactly, so it is recomputed per
+// candidate instead of being carried in a second register array.
+__device__ __forceinline__ int quest_exact(const float (&x)[32], int e_hi, int e_lo) {
     int best_e = e_hi;
     double best_err = -1.0;
     for (int e = e_hi; e >= e_lo; --e) {
+        const double sc = (double)exp2i(127 - e_hi) * (double)(1 << (e_hi - e));
         double acc = 0.0;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-            double a = fabs(vb[j]);
+            double a = fabs((double)x[j] * sc);
             double t = a - grid_round_d(a);
             acc = __dadd_rn(acc, __dmul_rn(t, t));
         }
@@ -47,8 +46,6 @@ __device__ __noinline__ int quest_exact(const float* x, int e_hi, int e_lo) {
             best_err = err;
             best_e = e;
         }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) vb[j] = vb[j] * 2.0;
     }
     return best_e;
 }
