@@ -84,6 +84,12 @@ QT_API uint64_t qt_derive_seed(const uint64_t* parts, int nparts);      /* rng.d
  * randomized Hadamard flips position p.  d_bits holds ceil(n/32) words. */
 QT_API int qt_sign_bits(uint32_t* d_bits, int64_t n, uint64_t xi, void* stream);
 
+/* Blockwise transform only (the kernels.fwht plugin entry, _native.pyx:353-379, with the
+ * randomized variant of hadamard.py:82-85): out[r, :] = prescale * FWHT32(x[r, :] (.) s), fp32,
+ * bit-identical to the reference's fp32 butterfly.  x and out are dense [rows, cols]. */
+QT_API int qt_fwht32(const float* x, float* out, int64_t rows, int64_t cols, int transform,
+                     const uint32_t* sign_bits, float prescale, void* stream);
+
 /* ---- general quantizers ---------------------------------------------------------------
  * qt_quant_rows: groups along the contiguous axis of x[rows, cols] (row stride ldx elements).
  *   transform (+ sign_bits for RANDOMIZED, indexed by column), then * prescale (1.0 or 0.75,
@@ -103,6 +109,17 @@ QT_API int qt_quant_cols(const void* x, int in_dtype, int64_t ldx, const uint8_t
                   const uint8_t* mx_sf, int64_t mx_katoms, int64_t rows, int64_t cols, int transform,
                   const uint32_t* sign_bits, float prescale, int rounding, uint64_t sr_seed, uint64_t counter_start,
                   uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, int* err, void* stream);
+
+/* qt_quant_dual: both backward dy operands from ONE read of x[rows, cols]:
+ *   row operand  [rows, cols] groups along cols (sign_bits by column, SR seed seed_rows,
+ *                stream position r*cols + c)           -- qlinear.py:214, 219, 225 (G)
+ *   col operand  [cols, rows] groups along rows (sign_bits by row, SR seed seed_cols,
+ *                stream position c*rows + r)           -- qlinear.py:234, 239, 245 (G_t) */
+QT_API int qt_quant_dual(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_t cols, int transform,
+                         const uint32_t* sign_bits, float prescale, int rounding, uint64_t seed_rows,
+                         uint64_t seed_cols, uint8_t* row_codes, int64_t row_ldc, uint8_t* row_sf,
+                         int64_t row_katoms, uint32_t* row_mask, uint8_t* col_codes, int64_t col_ldc,
+                         uint8_t* col_sf, int64_t col_katoms, int* err, void* stream);
 
 /* ---- named hot-path entry points (dense row-major inputs, ld == cols) ------------------- */
 

@@ -43,6 +43,13 @@ int qt_sign_bits(uint32_t* d_bits, int64_t n, uint64_t xi, void* stream) {
     return launch_signs(d_bits, n, xi, (cudaStream_t)stream);
 }
 
+int qt_fwht32(const float* x, float* out, int64_t rows, int64_t cols, int transform, const uint32_t* sign_bits,
+             float prescale, void* stream) {
+    if (cols % 32 != 0 || rows < 0) return QT_ERR_SHAPE;
+    if (transform < 0 || transform > 2 || (transform == QT_TRANSFORM_RANDOMIZED && !sign_bits)) return QT_ERR_ARG;
+    return launch_transform_rows(x, out, rows, cols, transform, sign_bits, prescale, (cudaStream_t)stream);
+}
+
 int qt_quant_rows(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_t cols, int transform,
                   const uint32_t* sign_bits, float prescale, int rounding, uint64_t sr_seed, uint64_t counter_start,
                   uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, uint32_t* mask, int* err, int* fallbacks,
@@ -76,7 +83,27 @@ int qt_quant_cols(const void* x, int in_dtype, int64_t ldx, const uint8_t* mx_co
     QuantCfg cfg{transform, sign_bits, prescale, rounding, sr_base_of(sr_seed), counter_start};
     QuantOut out{codes, ldc, sf, katoms, nullptr, err, nullptr};
     MxIn mx{mx_codes, mx_ldc, mx_sf, mx_katoms};
-    return launch_quant_cols(x, in_dtype, ldx, mx, rows, cols, cfg, out, (cudaStream_t)stream);
+    return launch_quant_tile(x, in_dtype, ldx, mx, rows, cols, nullptr, nullptr, &cfg, &out, (cudaStream_t)stream);
+}
+
+int qt_quant_dual(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_t cols, int transform,
+                  const uint32_t* sign_bits, float prescale, int rounding, uint64_t seed_rows, uint64_t seed_cols,
+                  uint8_t* row_codes, int64_t row_ldc, uint8_t* row_sf, int64_t row_katoms, uint32_t* row_mask,
+                  uint8_t* col_codes, int64_t col_ldc, uint8_t* col_sf, int64_t col_katoms, int* err, void* stream) {
+    if (rows % 32 != 0 || cols % 32 != 0) return QT_ERR_SHAPE;
+    if ((in_dtype != QT_IN_BF16 && in_dtype != QT_IN_F32) || rounding < 0 || rounding > 2 || transform < 0 ||
+        transform > 2)
+        return QT_ERR_ARG;
+    if (transform == QT_TRANSFORM_RANDOMIZED && !sign_bits) return QT_ERR_ARG;
+    int esz = in_dtype == QT_IN_BF16 ? 2 : 4;
+    if (!al16(x) || (ldx * esz) % 16 || !al16(row_codes) || row_ldc % 16 || !al16(col_codes) || col_ldc % 16)
+        return QT_ERR_ALIGN;
+    QuantCfg rc{transform, sign_bits, prescale, rounding, sr_base_of(seed_rows), 0};
+    QuantCfg cc{transform, sign_bits, prescale, rounding, sr_base_of(seed_cols), 0};
+    QuantOut ro{row_codes, row_ldc, row_sf, row_katoms, row_mask, err, nullptr};
+    QuantOut co{col_codes, col_ldc, col_sf, col_katoms, nullptr, err, nullptr};
+    MxIn mx{nullptr, 0, nullptr, 0};
+    return launch_quant_tile(x, in_dtype, ldx, mx, rows, cols, &rc, &ro, &cc, &co, (cudaStream_t)stream);
 }
 
 int qt_quant_fwd_quest(const void* x, int in_dtype, int64_t rows, int64_t cols, int hadamard, uint8_t* codes,

@@ -45,11 +45,14 @@ struct EpiParams {
     float scale;
 };
 
+int launch_transform_rows(const float* x, float* out, int64_t rows, int64_t cols, int transform,
+                          const uint32_t* sign_bits, float prescale, cudaStream_t st);
 int launch_signs(uint32_t* bits, int64_t n, uint64_t xi, cudaStream_t st);
 int launch_quant_rows(const void* x, int in_type, int64_t ldx, int64_t rows, int64_t cols, const QuantCfg& cfg,
                       const QuantOut& out, cudaStream_t st);
-int launch_quant_cols(const void* x, int in_type, int64_t ldx, const MxIn& mx, int64_t R, int64_t C,
-                      const QuantCfg& cfg, const QuantOut& out, cudaStream_t st);
+int launch_quant_tile(const void* x, int in_type, int64_t ldx, const MxIn& mx, int64_t R, int64_t C,
+                      const QuantCfg* row_cfg, const QuantOut* row_out, const QuantCfg* col_cfg,
+                      const QuantOut* col_out, cudaStream_t st);
 int launch_gemm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, int64_t a_katoms, const uint8_t* b, int64_t ldb,
                 const uint8_t* b_sf, int64_t b_katoms, int64_t M, int64_t N, int64_t K, const EpiParams& ep,
                 cudaStream_t st);

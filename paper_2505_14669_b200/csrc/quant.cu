@@ -1,11 +1,14 @@
 // quant.cu -- fused Hadamard + MXFP4 quantizer kernels (HBM-bound, one pass over the input).
 //
 //   k_signs        sign bitmap of the randomized Hadamard (rng.py:57-62, hadamard.py:77-85)
-//   k_quant_rows   groups along the contiguous axis: forward X / W (H32 + QuEST) and the
-//                  backward dy row operand (RHT32 + x0.75 + RTN/SR), qlinear.py:139-157, 213-228
-//   k_quant_cols   transposing quantizer: groups along the strided axis, input bf16/f32 or an
-//                  MXFP4 operand that is dequantized first (dy^T, deq(X_q)^T, deq(W_q)^T),
-//                  qlinear.py:213-248
+//   k_quant_rows   thread-per-group quantizer along the contiguous axis (forward X / W:
+//                  H32 + QuEST, qlinear.py:139-157)
+//   k_quant_tile   128 x 64 smem tile, up to two passes over the same data:
+//                    row pass  groups along the contiguous axis (dy -> G, qlinear.py:214-225)
+//                    col pass  groups along the strided axis = the transposed operand
+//                              (dy^T -> G_t, deq(X_q)^T -> X_t, deq(W_q)^T -> W_t,
+//                               qlinear.py:215, 234-246)
+//                  so the backward's two dy operands come from ONE read of dy.
 #include "launch.h"
 #include "quant.cuh"
 
@@ -26,158 +29,237 @@ __global__ void k_signs(uint32_t* bits, int64_t n, uint64_t base) {
     bits[w] = m;
 }
 
-__device__ __forceinline__ void apply_transform(float (&v)[32], const QuantCfg& cfg, int64_t grp) {
-    if (cfg.transform == kRandomized) {
-        uint32_t s = __ldg(cfg.sign_bits + grp);
+__device__ __forceinline__ void apply_transform(Grp& g, int transform, const uint32_t* sign_bits, int64_t grp,
+                                                float prescale) {
+    if (transform == kRandomized) flip_signs(g, __ldg(sign_bits + grp));
+    if (transform != kNone) fwht32(g);
+    if (prescale != 1.0f) scale_grp(g, prescale);
+}
+
+__device__ __forceinline__ void unpack_bf16x8(uint4 u, float* dst) {
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(__float_as_uint(v[j]) ^ (((s >> j) & 1u) << 31));
-    }
-    if (cfg.transform != kNone) fwht32(v);
-    if (cfg.prescale != 1.0f) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], cfg.prescale);
+    for (int t = 0; t < 4; ++t) {
+        dst[2 * t] = __uint_as_float(w[t] << 16);
+        dst[2 * t + 1] = __uint_as_float(w[t] & 0xFFFF0000u);
     }
 }
 
-// One thread per 32-element group of a row-major [rows, cols] input (cols % 32 == 0).
-template <int IN>
-__global__ void __launch_bounds__(256) k_quant_rows(const void* __restrict__ x, int64_t ldx, int64_t rows,
-                                                    int64_t cols, QuantCfg cfg, QuantOut out) {
+// ------------------------------------------------------------------------ k_quant_rows
+template <int IN, int ROUND>
+__global__ void __launch_bounds__(256, 3) k_quant_rows(const void* __restrict__ x, int64_t ldx, int64_t rows,
+                                                       int64_t cols, QuantCfg cfg, QuantOut out) {
     const int64_t gpr = cols / 32;
     const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (gid >= rows * gpr) return;
     const int64_t r = gid / gpr, grp = gid - r * gpr;
-    float v[32];
+    Grp g;
+    float tmp[8];
     if (IN == kInBF16) {
         const uint4* p = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(x) + r * ldx + grp * 32);
+        uint4 u[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) u[q] = __ldg(p + q);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            uint4 u = __ldg(p + q);
-            uint32_t w[4] = {u.x, u.y, u.z, u.w};
+            unpack_bf16x8(u[q], tmp);
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                v[q * 8 + 2 * t] = __uint_as_float(w[t] << 16);
-                v[q * 8 + 2 * t + 1] = __uint_as_float(w[t] & 0xFFFF0000u);
-            }
+            for (int t = 0; t < 8; ++t) g.v(q * 8 + t) = tmp[t];
         }
     } else {
         const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(x) + r * ldx + grp * 32);
+        float4 f[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) f[q] = __ldg(p + q);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            float4 f = __ldg(p + q);
-            v[4 * q] = f.x;
-            v[4 * q + 1] = f.y;
-            v[4 * q + 2] = f.z;
-            v[4 * q + 3] = f.w;
+            g.v(4 * q) = f[q].x;
+            g.v(4 * q + 1) = f[q].y;
+            g.v(4 * q + 2) = f[q].z;
+            g.v(4 * q + 3) = f[q].w;
         }
     }
-    apply_transform(v, cfg, grp);
-    GroupOut o = quantize_group(v, cfg.rounding, cfg.sr_base, cfg.counter_start + (uint64_t)(r * cols + grp * 32),
-                                out.err, out.fallbacks);
+    apply_transform(g, cfg.transform, cfg.sign_bits, grp, cfg.prescale);
+    GroupOut o = quantize_grp<ROUND>(g, cfg.sr_base, cfg.counter_start + (uint64_t)(r * cols + grp * 32), out.err,
+                                     out.fallbacks);
     *reinterpret_cast<uint4*>(out.codes + r * out.ldc + grp * 16) = o.codes;
     out.sf[sf_offset(r, grp, out.katoms)] = (uint8_t)o.sf;
     if (out.mask) out.mask[r * gpr + grp] = o.mask;
 }
 
-// Transposing quantizer.  Input M[R, C] (row-major), output Q(T(M^T)) as an MXFP4 operand of
-// shape [C, R] with groups along R.  CTA tile: 128 input rows x 64 input columns.
-//   warp w: columns (w % 2) * 32 + lane, input rows (w / 2) * 32 .. +31 (one output group)
-constexpr int kColTileR = 128, kColTileC = 64;
-
-__device__ __forceinline__ float e2m1_decode(uint32_t nib) {
-    uint32_t m = nib & 7u, e = m >> 1, mb = m & 1u;
-    uint32_t bits = e == 0 ? (mb ? 0x3F000000u : 0u) : (((e + 126u) << 23) | (mb << 22));
-    return __uint_as_float(bits | ((nib & 8u) << 28));
+// Transform only (kernels.fwht seam, hadamard.py:72-91): out = prescale * H32(x (.) s), fp32 out.
+__global__ void __launch_bounds__(256) k_transform_rows(const float* __restrict__ x, float* __restrict__ out,
+                                                       int64_t rows, int64_t cols, int transform,
+                                                       const uint32_t* sign_bits, float prescale) {
+    const int64_t gpr = cols / 32;
+    const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (gid >= rows * gpr) return;
+    const int64_t r = gid / gpr, grp = gid - r * gpr;
+    Grp g;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) g.v(j) = x[r * cols + grp * 32 + j];
+    apply_transform(g, transform, sign_bits, grp, prescale);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) out[r * cols + grp * 32 + j] = g.v(j);
 }
 
-template <int IN>
-__global__ void __launch_bounds__(256) k_quant_cols(const void* __restrict__ x, int64_t ldx, MxIn mx, int64_t R,
-                                                    int64_t C, QuantCfg cfg, QuantOut out) {
-    __shared__ float tile[kColTileR][kColTileC + 1];
-    __shared__ __align__(16) uint8_t ocodes[kColTileC][80];
-    __shared__ uint8_t osf[kColTileC][4];
+int launch_transform_rows(const float* x, float* out, int64_t rows, int64_t cols, int transform,
+                          const uint32_t* sign_bits, float prescale, cudaStream_t st) {
+    if (rows == 0 || cols == 0) return 0;
+    int64_t groups = rows * (cols / 32);
+    k_transform_rows<<<(unsigned)((groups + 255) / 256), 256, 0, st>>>(x, out, rows, cols, transform, sign_bits,
+                                                                        prescale);
+    return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------ k_quant_tile
+// Tile: 128 rows x 64 columns, held in smem as bf16 (ESZ = 2) or fp32 (ESZ = 4) in 16-byte chunks.
+// Chunk k of row r lives at physical chunk k ^ sw(r), sw(r) = ((r & 3) + (r >> 5)) & 3, which makes
+// the fill (consecutive chunks of a row), the row pass (4 rows x 2 groups per 8-lane phase) and the
+// col pass (one chunk of 4 rows 32 apart per load) bank-conflict free for bf16 tiles.
+constexpr int kTR = 128, kTC = 64;
+
+struct TileArgs {
+    const void* x;      // dense input (bf16 / fp32), row stride ldx
+    int64_t ldx;
+    MxIn mx;            // MXFP4 input (in_type kInMXFP4)
+    int64_t R, C;
+    QuantCfg row_cfg, col_cfg;
+    QuantOut row_out, col_out;
+};
+
+__device__ __forceinline__ int tile_sw(int r) { return ((r & 3) + (r >> 5)) & 3; }
+
+template <int IN, bool ROWS, bool COLS, int ROUND>
+__global__ void __launch_bounds__(256, 3) k_quant_tile(TileArgs a) {
+    constexpr int ESZ = IN == kInF32 ? 4 : 2;          // smem element bytes
+    constexpr int CPR = kTC * ESZ / 16;                  // 16-byte chunks per row: 8 or 16
+    __shared__ __align__(16) uint4 tile[kTR * CPR];
     const int tid = threadIdx.x;
-    const int64_t r0 = blockIdx.y * (int64_t)kColTileR, c0 = blockIdx.x * (int64_t)kColTileC;
-    const int nr = (int)(R - r0 < kColTileR ? R - r0 : kColTileR), nc = (int)(C - c0 < kColTileC ? C - c0 : kColTileC);
+    const int64_t r0 = blockIdx.x * (int64_t)kTR, c0 = blockIdx.y * (int64_t)kTC;
+    const int nr = (int)(a.R - r0 < kTR ? a.R - r0 : kTR), nc = (int)(a.C - c0 < kTC ? a.C - c0 : kTC);
 
-    // ---- load (coalesced along C) into fp32 smem
-    if (IN == kInBF16) {
-        const __nv_bfloat16* xb = static_cast<const __nv_bfloat16*>(x);
-        for (int i = tid; i < kColTileR * (kColTileC / 8); i += 256) {
-            int rr = i / (kColTileC / 8), cc = (i % (kColTileC / 8)) * 8;
-            if (rr < nr && cc < nc) {
-                uint4 u = __ldg(reinterpret_cast<const uint4*>(xb + (r0 + rr) * ldx + c0 + cc));
-                uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    // ---- fill
+    if (IN == kInMXFP4) {
+        // thread -> (row t/2, group t%2): 16 code bytes + 1 scale, decoded exactly to bf16
+        const int rr = tid >> 1, gg = tid & 1;
+        uint4 outc[4] = {};
+        if (rr < nr && gg * 32 < nc) {
+            const int64_t grow = r0 + rr, ggrp = c0 / 32 + gg;
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(a.mx.codes + grow * a.mx.ldc + ggrp * 16));
+            const uint32_t e = a.mx.sf[sf_offset(grow, ggrp, a.mx.katoms)];
+            const float s = exp2i((int)e - 127);
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    tile[rr][cc + 2 * t] = __uint_as_float(w[t] << 16);
-                    tile[rr][cc + 2 * t + 1] = __uint_as_float(w[t] & 0xFFFF0000u);
+            for (int q = 0; q < 4; ++q) {
+                uint32_t bw[4];
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    float2 f = e2m1x2_to_f32((w[q] >> (8 * b)) & 0xFFu);
+                    // code * 2^(e-127) is exact in fp32 and in bf16 (<= 3 significant bits)
+                    uint32_t lo = __float_as_uint(f.x * s) >> 16, hi = __float_as_uint(f.y * s) >> 16;
+                    bw[b] = lo | (hi << 16);
                 }
+                outc[q] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
             }
         }
-    } else if (IN == kInF32) {
-        const float* xf = static_cast<const float*>(x);
-        for (int i = tid; i < kColTileR * (kColTileC / 4); i += 256) {
-            int rr = i / (kColTileC / 4), cc = (i % (kColTileC / 4)) * 4;
-            if (rr < nr && cc < nc) {
-                float4 f = __ldg(reinterpret_cast<const float4*>(xf + (r0 + rr) * ldx + c0 + cc));
-                tile[rr][cc] = f.x;
-                tile[rr][cc + 1] = f.y;
-                tile[rr][cc + 2] = f.z;
-                tile[rr][cc + 3] = f.w;
-            }
-        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tile[rr * CPR + ((gg * 4 + q) ^ tile_sw(rr))] = outc[q];
     } else {
-        // MXFP4 operand [R, C] (groups along C): dequantize exactly, code * 2^(e-127) in fp32
-        // (codec.py:204-211 followed by the f32 cast of qlinear._values).
-        int rr = tid / 2, g = tid % 2;
-        if (rr < nr && g * 32 < nc) {
-            int64_t grow = r0 + rr, ggrp = c0 / 32 + g;
-            uint4 u = __ldg(reinterpret_cast<const uint4*>(mx.codes + grow * mx.ldc + ggrp * 16));
-            float s = exp2i((int)mx.sf[sf_offset(grow, ggrp, mx.katoms)] - 127);
-            uint32_t w[4] = {u.x, u.y, u.z, u.w};
+        const uint8_t* xb = static_cast<const uint8_t*>(a.x);
+        uint4 u[kTR * CPR / 256];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+        for (int it = 0; it < kTR * CPR / 256; ++it) {
+            const int id = it * 256 + tid, rr = id / CPR, k = id % CPR;
+            u[it] = make_uint4(0, 0, 0, 0);
+            if (rr < nr && k * (16 / ESZ) < nc)
+                u[it] = __ldg(reinterpret_cast<const uint4*>(xb + ((r0 + rr) * a.ldx + c0) * ESZ + k * 16));
+        }
 #pragma unroll
-                for (int n = 0; n < 8; ++n) tile[rr][g * 32 + q * 8 + n] = e2m1_decode(w[q] >> (4 * n)) * s;
+        for (int it = 0; it < kTR * CPR / 256; ++it) {
+            const int id = it * 256 + tid, rr = id / CPR, k = id % CPR;
+            tile[rr * CPR + (k ^ tile_sw(rr))] = u[it];
         }
     }
     __syncthreads();
 
-    // ---- one output group per thread
-    const int warp = tid / 32, lane = tid % 32;
-    const int cc = (warp % 2) * 32 + lane, q = warp / 2;
-    if (cc < nc && q * 32 < nr) {
-        float v[32];
+    // ---- row pass: thread -> (row t/2, group t%2)
+    if (ROWS) {
+        const int rr = tid >> 1, gg = tid & 1;
+        const bool ok = rr < nr && gg * 32 < nc;
+        Grp g;
+        if (ESZ == 2) {
+            float tmp[8];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = tile[q * 32 + i][cc];
-        const int64_t ogrp = r0 / 32 + q;  // group index along R
-        apply_transform(v, cfg, ogrp);
-        const int64_t orow = c0 + cc;
-        GroupOut o = quantize_group(v, cfg.rounding, cfg.sr_base, cfg.counter_start + (uint64_t)(orow * R + ogrp * 32),
-                                    out.err, out.fallbacks);
-        *reinterpret_cast<uint4*>(&ocodes[cc][q * 16]) = o.codes;
-        osf[cc][q] = (uint8_t)o.sf;
-        if (out.mask) out.mask[orow * (R / 32) + ogrp] = o.mask;
-    }
-    __syncthreads();
-
-    // ---- coalesced stores: each output row gets up to 64 contiguous code bytes + 4 SF bytes
-    {
-        int row = tid / 4, chunk = tid % 4;
-        if (row < nc && chunk * 32 < nr) {
-            int64_t orow = c0 + row;
-            *reinterpret_cast<uint4*>(out.codes + orow * out.ldc + (r0 / 32 + chunk) * 16) =
-                *reinterpret_cast<const uint4*>(&ocodes[row][chunk * 16]);
+            for (int q = 0; q < 4; ++q) {
+                unpack_bf16x8(tile[rr * CPR + ((gg * 4 + q) ^ tile_sw(rr))], tmp);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) g.v(q * 8 + t) = tmp[t];
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                uint4 u = tile[rr * CPR + ((gg * 8 + q) ^ tile_sw(rr))];
+                g.v(q * 4) = __uint_as_float(u.x);
+                g.v(q * 4 + 1) = __uint_as_float(u.y);
+                g.v(q * 4 + 2) = __uint_as_float(u.z);
+                g.v(q * 4 + 3) = __uint_as_float(u.w);
+            }
         }
-        if (tid < nc) {
-            int64_t orow = c0 + tid, g0 = r0 / 32;
-            int ng = (nr + 31) / 32;
-            if (ng == 4) {
-                uint32_t w = osf[tid][0] | (osf[tid][1] << 8) | (osf[tid][2] << 16) | ((uint32_t)osf[tid][3] << 24);
-                *reinterpret_cast<uint32_t*>(out.sf + sf_offset(orow, g0, out.katoms)) = w;
+        const int64_t row = r0 + rr, grp = c0 / 32 + gg;
+        GroupOut o;
+        o.sf = 0;
+        if (ok) {
+            apply_transform(g, a.row_cfg.transform, a.row_cfg.sign_bits, grp, a.row_cfg.prescale);
+            o = quantize_grp<ROUND>(g, a.row_cfg.sr_base, a.row_cfg.counter_start + (uint64_t)(row * a.C + grp * 32),
+                                    a.row_out.err, a.row_out.fallbacks);
+            *reinterpret_cast<uint4*>(a.row_out.codes + row * a.row_out.ldc + grp * 16) = o.codes;
+            if (a.row_out.mask) a.row_out.mask[row * (a.C / 32) + grp] = o.mask;
+        }
+        const uint32_t other = __shfl_xor_sync(0xffffffffu, o.sf, 1);
+        if (ok && gg == 0) {
+            if (nc > 32)  // groups grp, grp+1 are adjacent bytes of one atom word (grp even)
+                *reinterpret_cast<uint16_t*>(a.row_out.sf + sf_offset(row, grp, a.row_out.katoms)) =
+                    (uint16_t)(o.sf | (other << 8));
+            else
+                a.row_out.sf[sf_offset(row, grp, a.row_out.katoms)] = (uint8_t)o.sf;
+        }
+    }
+
+    // ---- col pass: thread -> (column t/4, row group t%4)
+    if (COLS) {
+        const int cc = tid >> 2, q = tid & 3;
+        const bool ok = cc < nc && q * 32 < nr;
+        Grp g;
+        const int k = cc / (16 / ESZ), off = cc % (16 / ESZ);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const int rr = q * 32 + i;
+            const uint8_t* base = reinterpret_cast<const uint8_t*>(&tile[rr * CPR + (k ^ tile_sw(rr))]);
+            if (ESZ == 2)
+                g.v(i) = __uint_as_float((uint32_t)(*reinterpret_cast<const uint16_t*>(base + off * 2)) << 16);
+            else
+                g.v(i) = *reinterpret_cast<const float*>(base + off * 4);
+        }
+        const int64_t orow = c0 + cc, ogrp = r0 / 32 + q;
+        GroupOut o;
+        o.sf = 0;
+        if (ok) {
+            apply_transform(g, a.col_cfg.transform, a.col_cfg.sign_bits, ogrp, a.col_cfg.prescale);
+            o = quantize_grp<ROUND>(g, a.col_cfg.sr_base, a.col_cfg.counter_start + (uint64_t)(orow * a.R + ogrp * 32),
+                                    a.col_out.err, a.col_out.fallbacks);
+            *reinterpret_cast<uint4*>(a.col_out.codes + orow * a.col_out.ldc + ogrp * 16) = o.codes;
+        }
+        // gather the 4 scale bytes of this column into lane q == 0 (one 32-bit atom word)
+        uint32_t sfw = o.sf << (8 * q);
+        sfw |= __shfl_xor_sync(0xffffffffu, sfw, 1);
+        sfw |= __shfl_xor_sync(0xffffffffu, sfw, 2);
+        if (ok && q == 0) {
+            if (nr == kTR) {
+                *reinterpret_cast<uint32_t*>(a.col_out.sf + sf_offset(orow, ogrp, a.col_out.katoms)) = sfw;
             } else {
-                for (int g = 0; g < ng; ++g) out.sf[sf_offset(orow, g0 + g, out.katoms)] = osf[tid][g];
+                for (int j = 0; j * 32 < nr; ++j)
+                    a.col_out.sf[sf_offset(orow, ogrp + j, a.col_out.katoms)] = (uint8_t)(sfw >> (8 * j));
             }
         }
     }
@@ -186,9 +268,8 @@ __global__ void __launch_bounds__(256) k_quant_cols(const void* __restrict__ x, 
 }  // namespace qt
 
 // ------------------------------------------------------------------------------- launchers
-using namespace qt;
-
 namespace qt {
+
 int launch_signs(uint32_t* bits, int64_t n, uint64_t xi, cudaStream_t st) {
     if (n <= 0) return 0;
     uint64_t base = mix64(xi ^ mix64(kDomainSigns));
@@ -197,28 +278,82 @@ int launch_signs(uint32_t* bits, int64_t n, uint64_t xi, cudaStream_t st) {
     return (int)cudaGetLastError();
 }
 
+template <int IN>
+static void rows_dispatch(const void* x, int64_t ldx, int64_t rows, int64_t cols, const QuantCfg& cfg,
+                          const QuantOut& out, unsigned grid, cudaStream_t st) {
+    if (cfg.rounding == kQuest)
+        k_quant_rows<IN, kQuest><<<grid, 256, 0, st>>>(x, ldx, rows, cols, cfg, out);
+    else if (cfg.rounding == kRtn)
+        k_quant_rows<IN, kRtn><<<grid, 256, 0, st>>>(x, ldx, rows, cols, cfg, out);
+    else
+        k_quant_rows<IN, kSr><<<grid, 256, 0, st>>>(x, ldx, rows, cols, cfg, out);
+}
+
 int launch_quant_rows(const void* x, int in_type, int64_t ldx, int64_t rows, int64_t cols, const QuantCfg& cfg,
                       const QuantOut& out, cudaStream_t st) {
     if (rows == 0 || cols == 0) return 0;
     int64_t groups = rows * (cols / 32);
     unsigned grid = (unsigned)((groups + 255) / 256);
     if (in_type == kInBF16)
-        k_quant_rows<kInBF16><<<grid, 256, 0, st>>>(x, ldx, rows, cols, cfg, out);
+        rows_dispatch<kInBF16>(x, ldx, rows, cols, cfg, out, grid, st);
     else
-        k_quant_rows<kInF32><<<grid, 256, 0, st>>>(x, ldx, rows, cols, cfg, out);
+        rows_dispatch<kInF32>(x, ldx, rows, cols, cfg, out, grid, st);
     return (int)cudaGetLastError();
 }
 
-int launch_quant_cols(const void* x, int in_type, int64_t ldx, const MxIn& mx, int64_t R, int64_t C,
-                      const QuantCfg& cfg, const QuantOut& out, cudaStream_t st) {
-    if (R == 0 || C == 0) return 0;
-    dim3 grid((unsigned)((C + kColTileC - 1) / kColTileC), (unsigned)((R + kColTileR - 1) / kColTileR));
-    if (in_type == kInBF16)
-        k_quant_cols<kInBF16><<<grid, 256, 0, st>>>(x, ldx, mx, R, C, cfg, out);
-    else if (in_type == kInF32)
-        k_quant_cols<kInF32><<<grid, 256, 0, st>>>(x, ldx, mx, R, C, cfg, out);
+template <int IN, bool ROWS, bool COLS>
+static void tile_round_dispatch(const TileArgs& a, int round, dim3 grid, cudaStream_t st) {
+    if (round == kRtn)
+        k_quant_tile<IN, ROWS, COLS, kRtn><<<grid, 256, 0, st>>>(a);
+    else if (round == kSr)
+        k_quant_tile<IN, ROWS, COLS, kSr><<<grid, 256, 0, st>>>(a);
     else
-        k_quant_cols<kInMXFP4><<<grid, 256, 0, st>>>(x, ldx, mx, R, C, cfg, out);
+        k_quant_tile<IN, ROWS, COLS, kQuest><<<grid, 256, 0, st>>>(a);
+}
+
+// Row and/or column passes over one read of x[R, C] (both passes share the rounding mode).
+int launch_quant_tile(const void* x, int in_type, int64_t ldx, const MxIn& mx, int64_t R, int64_t C,
+                      const QuantCfg* row_cfg, const QuantOut* row_out, const QuantCfg* col_cfg,
+                      const QuantOut* col_out, cudaStream_t st) {
+    if (R == 0 || C == 0) return 0;
+    const bool rows = row_cfg != nullptr, cols = col_cfg != nullptr;
+    if (!rows && !cols) return 0;
+    if (rows && cols && row_cfg->rounding != col_cfg->rounding) return 2003;
+    if (in_type == kInMXFP4 && rows) return 2003;  // MXFP4 input is only re-quantized transposed
+    TileArgs a{};
+    a.x = x;
+    a.ldx = ldx;
+    a.mx = mx;
+    a.R = R;
+    a.C = C;
+    if (rows) {
+        a.row_cfg = *row_cfg;
+        a.row_out = *row_out;
+    }
+    if (cols) {
+        a.col_cfg = *col_cfg;
+        a.col_out = *col_out;
+    }
+    const int round = rows ? row_cfg->rounding : col_cfg->rounding;
+    dim3 grid((unsigned)((R + kTR - 1) / kTR), (unsigned)((C + kTC - 1) / kTC));
+    if (in_type == kInMXFP4) {
+        tile_round_dispatch<kInMXFP4, false, true>(a, round, grid, st);
+    } else if (in_type == kInBF16) {
+        if (rows && cols)
+            tile_round_dispatch<kInBF16, true, true>(a, round, grid, st);
+        else if (rows)
+            tile_round_dispatch<kInBF16, true, false>(a, round, grid, st);
+        else
+            tile_round_dispatch<kInBF16, false, true>(a, round, grid, st);
+    } else {
+        if (rows && cols)
+            tile_round_dispatch<kInF32, true, true>(a, round, grid, st);
+        else if (rows)
+            tile_round_dispatch<kInF32, true, false>(a, round, grid, st);
+        else
+            tile_round_dispatch<kInF32, false, true>(a, round, grid, st);
+    }
     return (int)cudaGetLastError();
 }
+
 }  // namespace qt

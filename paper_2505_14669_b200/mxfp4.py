@@ -108,6 +108,18 @@ def sign_bits(xi: int, n: int, device) -> torch.Tensor:
     return out
 
 
+def fwht32(x: torch.Tensor, transform: int = 1, signs: torch.Tensor | None = None,
+           prescale: float = 1.0) -> torch.Tensor:
+    """prescale * FWHT32(x (.) s) along the last axis, fp32 (kernels.fwht, _native.pyx:353-379)."""
+    _require_cuda(x, "x")
+    x = x.contiguous().float()
+    out = torch.empty_like(x)
+    check(_lib.load().qt_fwht32(x.data_ptr(), out.data_ptr(), x.shape[0], x.shape[1], transform,
+                                signs.data_ptr() if signs is not None else None, float(prescale),
+                                _stream(x.device)), "qt_fwht32")
+    return out
+
+
 def quant_rows(x: torch.Tensor, transform: int, rounding: int, *, signs: torch.Tensor | None = None,
                prescale: float = 1.0, sr_seed: int = 0, counter_start: int = 0, want_mask: bool = False,
                err: torch.Tensor | None = None, fallbacks: torch.Tensor | None = None,
@@ -157,6 +169,28 @@ def quant_cols(x, rounding: int, *, transform: int, signs: torch.Tensor | None =
                          err.data_ptr() if err is not None else None, _stream(dev))
     check(rc, "qt_quant_cols")
     return op
+
+
+def quant_dual(x: torch.Tensor, rounding: int, *, transform: int, signs: torch.Tensor | None = None,
+               prescale: float = 1.0, seed_rows: int = 0, seed_cols: int = 0, err: torch.Tensor | None = None):
+    """Both backward dy operands from ONE read of x[rows, cols]: (rows-operand [rows, cols] grouped along
+    cols, cols-operand [cols, rows] grouped along rows) -- qlinear.py:214-245."""
+    _require_cuda(x, "x")
+    if x.stride(1) != 1:
+        x = x.contiguous()
+    rows, cols = x.shape
+    if rows % GROUP or cols % GROUP:
+        raise ValueError(f"dual quantization needs both axes divisible by {GROUP}: {rows}x{cols}")
+    r_op = MXOperand.empty(rows, cols, x.device)
+    c_op = MXOperand.empty(cols, rows, x.device)
+    rc = _lib.load().qt_quant_dual(x.data_ptr(), _in_dtype(x), x.stride(0), rows, cols, transform,
+                                   signs.data_ptr() if signs is not None else None, float(prescale), rounding,
+                                   int(seed_rows) & 0xFFFFFFFFFFFFFFFF, int(seed_cols) & 0xFFFFFFFFFFFFFFFF,
+                                   r_op.codes.data_ptr(), r_op.codes.stride(0), r_op.sf.data_ptr(), r_op.katoms, None,
+                                   c_op.codes.data_ptr(), c_op.codes.stride(0), c_op.sf.data_ptr(), c_op.katoms,
+                                   err.data_ptr() if err is not None else None, _stream(x.device))
+    check(rc, "qt_quant_dual")
+    return r_op, c_op
 
 
 def gemm(a: MXOperand, b: MXOperand, *, out_dtype=torch.float32, mask: torch.Tensor | None = None,

@@ -11,11 +11,10 @@ same argument meaning, same ValueError cases, same seeds / stream tags, bit-iden
 outputs.  Tensors are CUDA torch tensors; every step runs in libquartet_b200.so:
 
     forward : X_q, M_x = QuEST(H32(x));  W_q, M_w = QuEST(H32(w));  y = tcgen05(X_q, W_q)
-    dX      : G_q  = Q(H32(dy . s) * 3/4)          (qt_quant_bwd_rows)
-              Wt_q = Q(H32(deq(W_q)^T . s) * 3/4)  (qt_requant_t)
+    dy      : G_q  = Q(H32(dy . s) * 3/4),  Gt_q = Q(H32(dy^T . s) * 3/4)   (qt_quant_dual, one read)
+    dX      : Wt_q = Q(H32(deq(W_q)^T . s) * 3/4)  (qt_requant_t)
               dx   = H32(tcgen05(G_q, Wt_q) . M_x) * 16/9   (fused epilogue)
-    dW      : Gt_q = Q(H32(dy^T . s) * 3/4)        (qt_quant_bwd_cols)
-              Xt_q = Q(H32(deq(X_q)^T . s) * 3/4)  (qt_requant_t)
+    dW      : Xt_q = Q(H32(deq(X_q)^T . s) * 3/4)  (qt_requant_t)
               dw   = H32(tcgen05(Gt_q, Xt_q) . M_w) * 16/9
 
 Only the reference's default GemmPolicy (single accumulation, quantized operands) runs on the GPU;
@@ -29,7 +28,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from .mxfp4 import GROUP, MXOperand, derive_seed, gemm, quant_cols, quant_rows, sign_bits
+from .mxfp4 import GROUP, MXOperand, derive_seed, gemm, quant_cols, quant_dual, quant_rows, sign_bits
 
 PRE_SCALE = 0.75                     # qlinear.py:36
 POST_SCALE = 16.0 / 9.0              # qlinear.py:37
@@ -201,16 +200,17 @@ def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn"
     sr = rounding == "sr"
     err = _err_flag(dev) if check_finite else None
 
+    # both dy operands from one read of dy: G (rows, qlinear.py:214) and G_t (cols, qlinear.py:234)
+    g_q, gt_q = quant_dual(dy, rc, transform=transform, signs=signs, prescale=PRE_SCALE,
+                           seed_rows=derive_seed(xi, _TAG_BWD_G1) if sr else 0,
+                           seed_cols=derive_seed(xi, _TAG_BWD_G2) if sr else 0, err=err)
+
     # input gradient: contract over d_out (qlinear.py:212-230)
-    g_q = quant_rows(dy, transform, rc, signs=signs, prescale=PRE_SCALE,
-                     sr_seed=derive_seed(xi, _TAG_BWD_G1) if sr else 0, err=err)
     wt_q = quant_cols(ctx.w_q, rc, transform=transform, signs=signs, prescale=PRE_SCALE,
                       sr_seed=derive_seed(xi, _TAG_BWD_W) if sr else 0, err=err)
     dx = gemm(g_q, wt_q, out_dtype=dx_dtype, mask=ctx.x_q.mask, hadamard=ctx.hadamard, scale=_POST_F32)
 
     # weight gradient: contract over batch (qlinear.py:232-250)
-    gt_q = quant_cols(dy, rc, transform=transform, signs=signs, prescale=PRE_SCALE,
-                      sr_seed=derive_seed(xi, _TAG_BWD_G2) if sr else 0, err=err)
     xt_q = quant_cols(ctx.x_q, rc, transform=transform, signs=signs, prescale=PRE_SCALE,
                       sr_seed=derive_seed(xi, _TAG_BWD_X) if sr else 0, err=err)
     dw = gemm(gt_q, xt_q, out_dtype=dw_dtype, mask=ctx.w_q.mask, hadamard=ctx.hadamard, scale=_POST_F32)

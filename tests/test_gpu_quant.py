@@ -192,3 +192,41 @@ def test_sr_unbiased_known_answer(qt):
     vals = op.dequantize(torch.float64)[:, 1].cpu().numpy()
     assert set(np.unique(vals)) <= {2.0, 3.0}
     assert abs((vals == 3.0).mean() - 0.4) < 0.005
+
+
+@pytest.mark.parametrize("rounding", ["rtn", "sr"])
+@pytest.mark.parametrize("shape,dtype", [((256, 384), torch.bfloat16), ((160, 96), torch.bfloat16),
+                                         ((96, 224), torch.float32)])
+def test_dual_dy_quantizer(qt, oracle, rounding, shape, dtype):
+    """G_q and G_t from one read of dy (qlinear.py:214-245), both bit-exact."""
+    T, d_out = shape
+    xi = 13
+    dy = r = np.random.default_rng(7).normal(size=(T, d_out)).astype(np.float32)
+    if dtype == torch.bfloat16:
+        dy = bf16_values(dy)
+    signs = qt.sign_bits(xi, max(T, d_out), "cuda")
+    rc = qt._lib.QT_ROUND_RTN if rounding == "rtn" else qt._lib.QT_ROUND_SR
+    s_r, s_c = oracle.derive_seed(xi, 21), oracle.derive_seed(xi, 23)
+    g_op, gt_op = qt.quant_dual(to_dev(dy, dtype), rc, transform=qt._lib.QT_TRANSFORM_RANDOMIZED, signs=signs,
+                                prescale=0.75, seed_rows=s_r, seed_cols=s_c)
+    gh = oracle.fwht(dy * oracle.signs(xi, 0, d_out), 32) * np.float32(0.75)
+    gt = oracle.fwht(np.ascontiguousarray(dy.T) * oracle.signs(xi, 0, T), 32) * np.float32(0.75)
+    if rounding == "rtn":
+        (c1, s1), (c2, s2) = oracle.quantize_rtn(gh.astype(np.float64), 32), oracle.quantize_rtn(gt.astype(np.float64), 32)
+    else:
+        (c1, s1) = oracle.quantize_sr(gh.astype(np.float64), 32, s_r, 0)
+        (c2, s2) = oracle.quantize_sr(gt.astype(np.float64), 32, s_c, 0)
+    assert_operand_equal(g_op, c1, s1, "dual rows")
+    assert_operand_equal(gt_op, c2, s2, "dual cols")
+
+
+@pytest.mark.parametrize("prescale", [1.0, 0.75])
+def test_fwht32_bit_exact(qt, oracle, prescale):
+    """The packed f32x2 butterfly equals the reference's scalar fp32 butterfly bit for bit."""
+    r = np.random.default_rng(17)
+    x = (r.standard_t(df=3, size=(4096, 256)) * np.exp(r.normal(size=(4096, 1)))).astype(np.float32)
+    signs = qt.sign_bits(5, 256, "cuda")
+    got = qt.mxfp4.fwht32(to_dev(x), qt._lib.QT_TRANSFORM_RANDOMIZED, signs, prescale).cpu().numpy()
+    ref = oracle.fwht(x * oracle.signs(5, 0, 256), 32) * np.float32(prescale)
+    bad = np.argwhere(got.view(np.uint32) != ref.view(np.uint32))
+    assert bad.size == 0, (len(bad), bad[:3], got[tuple(bad[0])], ref[tuple(bad[0])])
