@@ -9,7 +9,11 @@ using namespace qt;
 static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 static inline uint64_t sr_base_of(uint64_t seed) { return mix64(seed ^ mix64(kDomainSR)); }
 
+static int g_gemm_dbg = 0;  // experiment knobs for qt_debug_set_gemm (never set in production)
+
 extern "C" {
+
+QT_API void qt_debug_set_gemm(int dbg) { g_gemm_dbg = dbg; }
 
 int qt_abi_version(void) { return QT_ABI_VERSION; }
 
@@ -146,7 +150,7 @@ int qt_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b_c
     if (epilogue != QT_EPI_STORE && !mask) return QT_ERR_ARG;
     int esz = out_dtype == QT_OUT_BF16 ? 2 : 4;
     if (!al16(a_codes) || !al16(b_codes) || !al16(out) || (ldo * esz) % 16) return QT_ERR_ALIGN;
-    EpiParams ep{out, ldo, out_dtype == QT_OUT_BF16, epilogue, mask, N / 32, scale};
+    EpiParams ep{out, ldo, out_dtype == QT_OUT_BF16, epilogue, mask, N / 32, scale, g_gemm_dbg};
     int rc = launch_gemm(a_codes, qt_codes_ld(K), a_sf, qt_sf_katoms(K), b_codes, qt_codes_ld(K), b_sf,
                          qt_sf_katoms(K), M, N, K, ep, (cudaStream_t)stream);
     return rc == 1001 || rc == 1002 ? QT_ERR_TMA : rc;

@@ -43,6 +43,7 @@ struct EpiParams {
     const uint32_t* mask;    // [M, N/32] words (kEpiMaskH)
     int64_t ldm;             // words per mask row
     float scale;
+    int dbg;                 // experiment knobs (0 in production)
 };
 
 int launch_transform_rows(const float* x, float* out, int64_t rows, int64_t cols, int transform,

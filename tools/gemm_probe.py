@@ -1,0 +1,36 @@
+"""GEMM mainloop experiments (timing only; results are wrong for dbg != 0)."""
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2505_14669_b200 as qt  # noqa: E402
+from paper_2505_14669_b200 import _lib  # noqa: E402
+
+L = qt.load()
+L.qt_debug_set_gemm.argtypes = [ctypes.c_int]
+dev = "cuda"
+for (M, N, K) in [(16384, 4096, 4096), (16384, 4096, 16384)]:
+    x = torch.randn(M, K, device=dev).to(torch.bfloat16)
+    w = torch.randn(N, K, device=dev).to(torch.bfloat16)
+    A = qt.quant_rows(x, 0, _lib.QT_ROUND_RTN)
+    B = qt.quant_rows(w, 0, _lib.QT_ROUND_RTN)
+    out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    for dbg, name in [(0, "baseline"), (1, "no SF tcgen05.cp after k0"), (3, "no SF loads+cp after k0"),
+                      (4, "1 MMA per k-tile (1/4 math)"), (8, "no B TMA after k0"), (12, "no B + 1 MMA"),
+                      (11, "no B, no SF")]:
+        L.qt_debug_set_gemm(dbg)
+        for _ in range(3):
+            qt.gemm(A, B, out=out)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(10):
+            qt.gemm(A, B, out=out)
+        e.record()
+        torch.cuda.synchronize()
+        us = s.elapsed_time(e) * 100
+        print(f"M{M} N{N} K{K} {name:32s} {us:8.1f} us  {2 * M * N * K / us / 1e6:7.1f} TF")
+    L.qt_debug_set_gemm(0)
