@@ -357,8 +357,8 @@ def run_ours(args, rank, world, local_rank):
                                "share_of_step": round(q_us * 1e-3 / ms, 4)},
         "kernels": table,
         "e2e": e2e,
-        # per step and shape: 2 forward quantizers + 1 GEMM; 1 sign bitmap + 1 dual + 2 requant + 2 GEMMs
-        "gpu_launches": 9 * len(SHAPES) * args.steps,
+        # per step and shape: 2 forward quantizers + 1 GEMM; 2 sign bitmaps + 1 dual + 2 requant + 2 GEMMs
+        "gpu_launches": 10 * len(SHAPES) * args.steps,
         "clocks": clocks,
     }
 

@@ -83,6 +83,8 @@ QT_API uint64_t qt_derive_seed(const uint64_t* parts, int nparts);      /* rng.d
 /* Sign bitmap of rng.signs(xi, 0, n) (rng.py:57-62): bit p%32 of word p/32 is 1 where the
  * randomized Hadamard flips position p.  d_bits holds ceil(n/32) words. */
 QT_API int qt_sign_bits(uint32_t* d_bits, int64_t n, uint64_t xi, void* stream);
+/* Same for rng.signs(xi, start, n): positions start .. start+n-1 (data-parallel token shards). */
+QT_API int qt_sign_bits_at(uint32_t* d_bits, int64_t start, int64_t n, uint64_t xi, void* stream);
 
 /* Blockwise transform only (the kernels.fwht plugin entry, _native.pyx:353-379, with the
  * randomized variant of hadamard.py:82-85): out[r, :] = prescale * FWHT32(x[r, :] (.) s), fp32,
@@ -102,24 +104,30 @@ QT_API int qt_quant_rows(const void* x, int in_dtype, int64_t ldx, int64_t rows,
                   int* fallbacks, void* stream);
 
 /* qt_quant_cols: quantize the TRANSPOSE of x[rows, cols]: output operand [cols, rows] with groups
- *   along `rows`; sign_bits indexed by row; SR stream position counter_start + c*rows + r.
+ *   along `rows`; sign_bits indexed by row; SR stream position counter_start + c*ld + r with
+ *   ld = counter_ld (0 -> rows; a token shard of a larger matrix passes the full length).
  *   in_dtype QT_IN_MXFP4 reads x as an MXFP4 operand (mx_codes/mx_ldc/mx_sf/mx_katoms; x unused)
  *   and dequantizes it exactly first (qlinear._values, qlinear.py:90-93). */
 QT_API int qt_quant_cols(const void* x, int in_dtype, int64_t ldx, const uint8_t* mx_codes, int64_t mx_ldc,
                   const uint8_t* mx_sf, int64_t mx_katoms, int64_t rows, int64_t cols, int transform,
                   const uint32_t* sign_bits, float prescale, int rounding, uint64_t sr_seed, uint64_t counter_start,
-                  uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, int* err, void* stream);
+                  int64_t counter_ld, uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, int* err,
+                  void* stream);
 
 /* qt_quant_dual: both backward dy operands from ONE read of x[rows, cols]:
- *   row operand  [rows, cols] groups along cols (sign_bits by column, SR seed seed_rows,
- *                stream position r*cols + c)           -- qlinear.py:214, 219, 225 (G)
- *   col operand  [cols, rows] groups along rows (sign_bits by row, SR seed seed_cols,
- *                stream position c*rows + r)           -- qlinear.py:234, 239, 245 (G_t) */
+ *   row operand  [rows, cols] groups along cols (row_sign_bits by column, SR seed seed_rows,
+ *                stream position row_counter_start + r*cols + c)          -- qlinear.py:214, 219, 225
+ *   col operand  [cols, rows] groups along rows (col_sign_bits by row, SR seed seed_cols,
+ *                stream position col_counter_start + c*ld + r, ld = col_counter_ld or rows)
+ *                                                                        -- qlinear.py:234, 239, 245
+ * A data-parallel token shard passes global sign offsets / counters so that its operands equal the
+ * corresponding slices of the single-GPU operands. */
 QT_API int qt_quant_dual(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_t cols, int transform,
-                         const uint32_t* sign_bits, float prescale, int rounding, uint64_t seed_rows,
-                         uint64_t seed_cols, uint8_t* row_codes, int64_t row_ldc, uint8_t* row_sf,
-                         int64_t row_katoms, uint32_t* row_mask, uint8_t* col_codes, int64_t col_ldc,
-                         uint8_t* col_sf, int64_t col_katoms, int* err, void* stream);
+                         const uint32_t* row_sign_bits, const uint32_t* col_sign_bits, float prescale, int rounding,
+                         uint64_t seed_rows, uint64_t row_counter_start, uint64_t seed_cols,
+                         uint64_t col_counter_start, int64_t col_counter_ld, uint8_t* row_codes, int64_t row_ldc,
+                         uint8_t* row_sf, int64_t row_katoms, uint32_t* row_mask, uint8_t* col_codes,
+                         int64_t col_ldc, uint8_t* col_sf, int64_t col_katoms, int* err, void* stream);
 
 /* ---- named hot-path entry points (dense row-major inputs, ld == cols) ------------------- */
 
@@ -146,6 +154,9 @@ QT_API int qt_requant_t(const uint8_t* codes, const uint8_t* sf, int64_t rows, i
 QT_API int qt_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b_codes, const uint8_t* b_sf,
                  int64_t M, int64_t N, int64_t K, void* out, int out_dtype, int64_t ldo, int epilogue,
                  const uint32_t* mask, float scale, void* stream);
+
+/* Experiment hook for the GEMM mainloop studies in tools/gemm_probe.py (0 = production). */
+QT_API void qt_debug_set_gemm(int dbg);
 
 #ifdef __cplusplus
 }

@@ -13,7 +13,7 @@ static int g_gemm_dbg = 0;  // experiment knobs for qt_debug_set_gemm (never set
 
 extern "C" {
 
-QT_API void qt_debug_set_gemm(int dbg) { g_gemm_dbg = dbg; }
+void qt_debug_set_gemm(int dbg) { g_gemm_dbg = dbg; }
 
 int qt_abi_version(void) { return QT_ABI_VERSION; }
 
@@ -44,7 +44,12 @@ uint64_t qt_derive_seed(const uint64_t* parts, int nparts) {
 }
 
 int qt_sign_bits(uint32_t* d_bits, int64_t n, uint64_t xi, void* stream) {
-    return launch_signs(d_bits, n, xi, (cudaStream_t)stream);
+    return launch_signs(d_bits, 0, n, xi, (cudaStream_t)stream);
+}
+
+int qt_sign_bits_at(uint32_t* d_bits, int64_t start, int64_t n, uint64_t xi, void* stream) {
+    if (start < 0) return QT_ERR_ARG;
+    return launch_signs(d_bits, start, n, xi, (cudaStream_t)stream);
 }
 
 int qt_fwht32(const float* x, float* out, int64_t rows, int64_t cols, int transform, const uint32_t* sign_bits,
@@ -64,7 +69,7 @@ int qt_quant_rows(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_
     if (transform == QT_TRANSFORM_RANDOMIZED && !sign_bits) return QT_ERR_ARG;
     int esz = in_dtype == QT_IN_BF16 ? 2 : 4;
     if (!al16(x) || (ldx * esz) % 16 || !al16(codes) || ldc % 16) return QT_ERR_ALIGN;
-    QuantCfg cfg{transform, sign_bits, prescale, rounding, sr_base_of(sr_seed), counter_start};
+    QuantCfg cfg{transform, sign_bits, prescale, rounding, sr_base_of(sr_seed), counter_start, 0};
     QuantOut out{codes, ldc, sf, katoms, mask, err, fallbacks};
     return launch_quant_rows(x, in_dtype, ldx, rows, cols, cfg, out, (cudaStream_t)stream);
 }
@@ -72,7 +77,8 @@ int qt_quant_rows(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_
 int qt_quant_cols(const void* x, int in_dtype, int64_t ldx, const uint8_t* mx_codes, int64_t mx_ldc,
                   const uint8_t* mx_sf, int64_t mx_katoms, int64_t rows, int64_t cols, int transform,
                   const uint32_t* sign_bits, float prescale, int rounding, uint64_t sr_seed, uint64_t counter_start,
-                  uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, int* err, void* stream) {
+                  int64_t counter_ld, uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, int* err,
+                  void* stream) {
     if (rows % 32 != 0 || cols % 32 != 0) return QT_ERR_SHAPE;
     if (in_dtype < 0 || in_dtype > 2 || rounding < 0 || rounding > 2 || transform < 0 || transform > 2)
         return QT_ERR_ARG;
@@ -84,26 +90,29 @@ int qt_quant_cols(const void* x, int in_dtype, int64_t ldx, const uint8_t* mx_co
         if (!al16(x) || (ldx * esz) % 16) return QT_ERR_ALIGN;
     }
     if (!al16(codes) || ldc % 16) return QT_ERR_ALIGN;
-    QuantCfg cfg{transform, sign_bits, prescale, rounding, sr_base_of(sr_seed), counter_start};
+    QuantCfg cfg{transform, sign_bits, prescale, rounding, sr_base_of(sr_seed), counter_start, counter_ld};
     QuantOut out{codes, ldc, sf, katoms, nullptr, err, nullptr};
     MxIn mx{mx_codes, mx_ldc, mx_sf, mx_katoms};
     return launch_quant_tile(x, in_dtype, ldx, mx, rows, cols, nullptr, nullptr, &cfg, &out, (cudaStream_t)stream);
 }
 
 int qt_quant_dual(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_t cols, int transform,
-                  const uint32_t* sign_bits, float prescale, int rounding, uint64_t seed_rows, uint64_t seed_cols,
-                  uint8_t* row_codes, int64_t row_ldc, uint8_t* row_sf, int64_t row_katoms, uint32_t* row_mask,
-                  uint8_t* col_codes, int64_t col_ldc, uint8_t* col_sf, int64_t col_katoms, int* err, void* stream) {
+                  const uint32_t* row_sign_bits, const uint32_t* col_sign_bits, float prescale, int rounding,
+                  uint64_t seed_rows, uint64_t row_counter_start, uint64_t seed_cols, uint64_t col_counter_start,
+                  int64_t col_counter_ld, uint8_t* row_codes, int64_t row_ldc, uint8_t* row_sf, int64_t row_katoms,
+                  uint32_t* row_mask, uint8_t* col_codes, int64_t col_ldc, uint8_t* col_sf, int64_t col_katoms,
+                  int* err, void* stream) {
     if (rows % 32 != 0 || cols % 32 != 0) return QT_ERR_SHAPE;
     if ((in_dtype != QT_IN_BF16 && in_dtype != QT_IN_F32) || rounding < 0 || rounding > 2 || transform < 0 ||
         transform > 2)
         return QT_ERR_ARG;
-    if (transform == QT_TRANSFORM_RANDOMIZED && !sign_bits) return QT_ERR_ARG;
+    if (transform == QT_TRANSFORM_RANDOMIZED && (!row_sign_bits || !col_sign_bits)) return QT_ERR_ARG;
     int esz = in_dtype == QT_IN_BF16 ? 2 : 4;
     if (!al16(x) || (ldx * esz) % 16 || !al16(row_codes) || row_ldc % 16 || !al16(col_codes) || col_ldc % 16)
         return QT_ERR_ALIGN;
-    QuantCfg rc{transform, sign_bits, prescale, rounding, sr_base_of(seed_rows), 0};
-    QuantCfg cc{transform, sign_bits, prescale, rounding, sr_base_of(seed_cols), 0};
+    QuantCfg rc{transform, row_sign_bits, prescale, rounding, sr_base_of(seed_rows), row_counter_start, 0};
+    QuantCfg cc{transform, col_sign_bits, prescale, rounding, sr_base_of(seed_cols), col_counter_start,
+                col_counter_ld};
     QuantOut ro{row_codes, row_ldc, row_sf, row_katoms, row_mask, err, nullptr};
     QuantOut co{col_codes, col_ldc, col_sf, col_katoms, nullptr, err, nullptr};
     MxIn mx{nullptr, 0, nullptr, 0};
@@ -130,7 +139,7 @@ int qt_quant_bwd_cols(const void* dy, int in_dtype, int64_t rows, int64_t cols, 
     if (rounding == QT_ROUND_QUEST) return QT_ERR_ARG;
     return qt_quant_cols(dy, in_dtype, cols, nullptr, 0, nullptr, 0, rows, cols,
                          sign_bits ? QT_TRANSFORM_RANDOMIZED : QT_TRANSFORM_NONE, sign_bits, 0.75f, rounding, sr_seed,
-                         0, codes, qt_codes_ld(rows), sf, qt_sf_katoms(rows), err, stream);
+                         0, 0, codes, qt_codes_ld(rows), sf, qt_sf_katoms(rows), err, stream);
 }
 
 int qt_requant_t(const uint8_t* codes, const uint8_t* sf, int64_t rows, int64_t cols, const uint32_t* sign_bits,
@@ -138,7 +147,7 @@ int qt_requant_t(const uint8_t* codes, const uint8_t* sf, int64_t rows, int64_t 
     if (rounding == QT_ROUND_QUEST) return QT_ERR_ARG;
     return qt_quant_cols(nullptr, QT_IN_MXFP4, 0, codes, qt_codes_ld(cols), sf, qt_sf_katoms(cols), rows, cols,
                          sign_bits ? QT_TRANSFORM_RANDOMIZED : QT_TRANSFORM_NONE, sign_bits, 0.75f, rounding, sr_seed,
-                         0, out_codes, qt_codes_ld(rows), out_sf, qt_sf_katoms(rows), err, stream);
+                         0, 0, out_codes, qt_codes_ld(rows), out_sf, qt_sf_katoms(rows), err, stream);
 }
 
 int qt_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b_codes, const uint8_t* b_sf, int64_t M,

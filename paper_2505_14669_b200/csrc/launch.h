@@ -26,6 +26,7 @@ struct QuantCfg {
     int rounding;
     uint64_t sr_base;           // mix64(seed ^ mix64(DOMAIN_SR))
     uint64_t counter_start;
+    int64_t counter_ld;         // SR stream row stride (0 = the quantized matrix's own row length)
 };
 
 struct MxIn {
@@ -48,7 +49,7 @@ struct EpiParams {
 
 int launch_transform_rows(const float* x, float* out, int64_t rows, int64_t cols, int transform,
                           const uint32_t* sign_bits, float prescale, cudaStream_t st);
-int launch_signs(uint32_t* bits, int64_t n, uint64_t xi, cudaStream_t st);
+int launch_signs(uint32_t* bits, int64_t start, int64_t n, uint64_t xi, cudaStream_t st);
 int launch_quant_rows(const void* x, int in_type, int64_t ldx, int64_t rows, int64_t cols, const QuantCfg& cfg,
                       const QuantOut& out, cudaStream_t st);
 int launch_quant_tile(const void* x, int in_type, int64_t ldx, const MxIn& mx, int64_t R, int64_t C,

@@ -16,7 +16,7 @@
 
 namespace qt {
 
-__global__ void k_signs(uint32_t* bits, int64_t n, uint64_t base) {
+__global__ void k_signs(uint32_t* bits, int64_t start, int64_t n, uint64_t base) {
     int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t nw = (n + 31) / 32;
     if (w >= nw) return;
@@ -24,7 +24,7 @@ __global__ void k_signs(uint32_t* bits, int64_t n, uint64_t base) {
     for (int j = 0; j < 32; ++j) {
         int64_t p = w * 32 + j;
         if (p < n) {
-            uint64_t h = mix64(base + ((uint64_t)p + 1) * kGolden);
+            uint64_t h = mix64(base + ((uint64_t)(start + p) + 1) * kGolden);
             m |= (uint32_t)(h >> 63) << j;
         }
     }
@@ -222,7 +222,8 @@ __device__ __forceinline__ void tile_row_pass(const TileArgs& a, const uint4* ti
         const QuantCfg& cf = a.row_cfg;
         transform_pair(g, cf.transform, cf.transform == kRandomized ? __ldg(cf.sign_bits + gA) : 0u,
                        cf.transform == kRandomized && okB ? __ldg(cf.sign_bits + gA + 1) : 0u, cf.prescale);
-        const uint64_t idx = cf.counter_start + (uint64_t)(row * a.C + gA * 32);
+        const int64_t cld = cf.counter_ld ? cf.counter_ld : a.C;
+        const uint64_t idx = cf.counter_start + (uint64_t)(row * cld + gA * 32);
         o = quantize_pair<ROUND>(g, cf.sr_base, idx, idx + 32, a.row_out.err, a.row_out.fallbacks);
         if (!okB) o.sf[1] = 0;
         uint8_t* cp = a.row_out.codes + row * a.row_out.ldc + gA * 16;
@@ -276,8 +277,9 @@ __device__ __forceinline__ void tile_col_pass(const TileArgs& a, const uint4* ti
         const QuantCfg& cf = a.col_cfg;
         const uint32_t s = cf.transform == kRandomized ? __ldg(cf.sign_bits + ogrp) : 0u;
         transform_pair(g, cf.transform, s, s, cf.prescale);
-        const uint64_t idx = cf.counter_start + (uint64_t)(orow * a.R + ogrp * 32);
-        o = quantize_pair<ROUND>(g, cf.sr_base, idx, idx + (uint64_t)a.R, a.col_out.err, a.col_out.fallbacks);
+        const int64_t cld = cf.counter_ld ? cf.counter_ld : a.R;
+        const uint64_t idx = cf.counter_start + (uint64_t)(orow * cld + ogrp * 32);
+        o = quantize_pair<ROUND>(g, cf.sr_base, idx, idx + (uint64_t)cld, a.col_out.err, a.col_out.fallbacks);
         *reinterpret_cast<uint4*>(a.col_out.codes + orow * a.col_out.ldc + ogrp * 16) = o.codes[0];
         *reinterpret_cast<uint4*>(a.col_out.codes + (orow + 1) * a.col_out.ldc + ogrp * 16) = o.codes[1];
     }
@@ -334,11 +336,11 @@ __global__ void __launch_bounds__(256, IN == kInF32 ? 1 : 2) k_quant_tile(TileAr
 // ------------------------------------------------------------------------------- launchers
 namespace qt {
 
-int launch_signs(uint32_t* bits, int64_t n, uint64_t xi, cudaStream_t st) {
+int launch_signs(uint32_t* bits, int64_t start, int64_t n, uint64_t xi, cudaStream_t st) {
     if (n <= 0) return 0;
     uint64_t base = mix64(xi ^ mix64(kDomainSigns));
     int64_t nw = (n + 31) / 32;
-    k_signs<<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(bits, n, base);
+    k_signs<<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(bits, start, n, base);
     return (int)cudaGetLastError();
 }
 

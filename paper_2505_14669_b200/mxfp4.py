@@ -100,11 +100,11 @@ def derive_seed(*parts: int) -> int:
     return int(_lib.load().qt_derive_seed(ctypes.cast(arr, ctypes.c_void_p), len(parts)))
 
 
-def sign_bits(xi: int, n: int, device) -> torch.Tensor:
-    """Device bitmap of rng.signs(xi, 0, n): int32 [ceil(n/32)]."""
+def sign_bits(xi: int, n: int, device, start: int = 0) -> torch.Tensor:
+    """Device bitmap of rng.signs(xi, start, n) (rng.py:57-62): int32 [ceil(n/32)]."""
     out = torch.empty(((n + 31) // 32,), dtype=torch.int32, device=device)
-    check(_lib.load().qt_sign_bits(out.data_ptr(), n, int(xi) & 0xFFFFFFFFFFFFFFFF, _stream(out.device)),
-          "qt_sign_bits")
+    check(_lib.load().qt_sign_bits_at(out.data_ptr(), int(start), n, int(xi) & 0xFFFFFFFFFFFFFFFF,
+                                      _stream(out.device)), "qt_sign_bits_at")
     return out
 
 
@@ -146,7 +146,7 @@ def quant_rows(x: torch.Tensor, transform: int, rounding: int, *, signs: torch.T
 
 
 def quant_cols(x, rounding: int, *, transform: int, signs: torch.Tensor | None = None, prescale: float = 1.0,
-               sr_seed: int = 0, counter_start: int = 0, err: torch.Tensor | None = None,
+               sr_seed: int = 0, counter_start: int = 0, counter_ld: int = 0, err: torch.Tensor | None = None,
                out: MXOperand | None = None) -> MXOperand:
     """Quantize the transpose of x ([rows, cols] dense tensor or MXOperand) along `rows`."""
     L = _lib.load()
@@ -165,16 +165,20 @@ def quant_cols(x, rounding: int, *, transform: int, signs: torch.Tensor | None =
     op = out if out is not None else MXOperand.empty(cols, rows, dev)
     rc = L.qt_quant_cols(*args, rows, cols, transform, signs.data_ptr() if signs is not None else None,
                          float(prescale), rounding, int(sr_seed) & 0xFFFFFFFFFFFFFFFF, int(counter_start),
-                         op.codes.data_ptr(), op.codes.stride(0), op.sf.data_ptr(), op.katoms,
+                         int(counter_ld), op.codes.data_ptr(), op.codes.stride(0), op.sf.data_ptr(), op.katoms,
                          err.data_ptr() if err is not None else None, _stream(dev))
     check(rc, "qt_quant_cols")
     return op
 
 
 def quant_dual(x: torch.Tensor, rounding: int, *, transform: int, signs: torch.Tensor | None = None,
-               prescale: float = 1.0, seed_rows: int = 0, seed_cols: int = 0, err: torch.Tensor | None = None):
+               col_signs: torch.Tensor | None = None, prescale: float = 1.0, seed_rows: int = 0, seed_cols: int = 0,
+               row_counter_start: int = 0, col_counter_start: int = 0, col_counter_ld: int = 0,
+               err: torch.Tensor | None = None):
     """Both backward dy operands from ONE read of x[rows, cols]: (rows-operand [rows, cols] grouped along
-    cols, cols-operand [cols, rows] grouped along rows) -- qlinear.py:214-245."""
+    cols, cols-operand [cols, rows] grouped along rows) -- qlinear.py:214-245.  `signs` flips the column
+    axis of the rows-operand, `col_signs` (default: `signs`) the row axis of the cols-operand."""
+    col_signs = signs if col_signs is None else col_signs
     _require_cuda(x, "x")
     if x.stride(1) != 1:
         x = x.contiguous()
@@ -184,8 +188,10 @@ def quant_dual(x: torch.Tensor, rounding: int, *, transform: int, signs: torch.T
     r_op = MXOperand.empty(rows, cols, x.device)
     c_op = MXOperand.empty(cols, rows, x.device)
     rc = _lib.load().qt_quant_dual(x.data_ptr(), _in_dtype(x), x.stride(0), rows, cols, transform,
-                                   signs.data_ptr() if signs is not None else None, float(prescale), rounding,
-                                   int(seed_rows) & 0xFFFFFFFFFFFFFFFF, int(seed_cols) & 0xFFFFFFFFFFFFFFFF,
+                                   signs.data_ptr() if signs is not None else None,
+                                   col_signs.data_ptr() if col_signs is not None else None, float(prescale), rounding,
+                                   int(seed_rows) & 0xFFFFFFFFFFFFFFFF, int(row_counter_start),
+                                   int(seed_cols) & 0xFFFFFFFFFFFFFFFF, int(col_counter_start), int(col_counter_ld),
                                    r_op.codes.data_ptr(), r_op.codes.stride(0), r_op.sf.data_ptr(), r_op.katoms, None,
                                    c_op.codes.data_ptr(), c_op.codes.stride(0), c_op.sf.data_ptr(), c_op.katoms,
                                    err.data_ptr() if err is not None else None, _stream(x.device))

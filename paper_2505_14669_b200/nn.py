@@ -44,9 +44,12 @@ class QuartetLinearFn(torch.autograd.Function):
         dy2 = dy.reshape(-1, dy.shape[-1])
         if dy2.dtype not in (torch.bfloat16, torch.float32):
             dy2 = dy2.float()
+        from .dp import ShardContext
+
         dx, dw = qlinear.backward(dy2, ctx.lctx, ctx.xi, ctx.rounding, dx_dtype=ctx.x_dtype
                                   if ctx.x_dtype in (torch.bfloat16, torch.float32) else torch.float32,
-                                  dw_dtype=torch.float32, check_finite=False)
+                                  dw_dtype=torch.float32, check_finite=False, token_offset=ShardContext.offset,
+                                  total_tokens=ShardContext.total)
         ctx.lctx = None
         return dx.reshape(ctx.x_shape), dw.to(ctx.w_dtype), None, None, None, None
 

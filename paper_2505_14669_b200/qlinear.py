@@ -182,8 +182,16 @@ def _rounding_code(rounding: str) -> int:
 
 def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn",
              dx_dtype: torch.dtype = torch.float32, dw_dtype: torch.dtype = torch.float32,
-             check_finite: bool = True, return_operands: bool = False):
-    """Input and weight gradients from the saved context and upstream dy (qlinear.py:178-252)."""
+             check_finite: bool = True, return_operands: bool = False, token_offset: int = 0,
+             total_tokens: int | None = None):
+    """Input and weight gradients from the saved context and upstream dy (qlinear.py:178-252).
+
+    Data-parallel shards: a rank holding tokens [token_offset, token_offset + batch) of a global batch of
+    `total_tokens` passes both; its randomized-Hadamard signs and stochastic-rounding stream positions
+    along the token axis are then the global ones, so its G / G_t / X_t operands are exactly the
+    corresponding slices of the single-GPU operands, its dx rows are exactly the single-GPU dx rows,
+    and the sum of the ranks' dw equals the single-GPU dw up to fp32 summation order (the masked
+    Hadamard epilogue is linear).  token_offset must be a multiple of 32."""
     if rounding not in ("exact", "rtn", "sr"):
         raise ValueError(f"unknown backward rounding {rounding!r}")
     rc = _rounding_code(rounding)
@@ -194,25 +202,32 @@ def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn"
         raise ValueError(f"output dimension {ctx.d_out} not divisible by block size {g}")
     if ctx.batch % g != 0:
         raise ValueError(f"batch size {ctx.batch} not divisible by block size {g}")
+    total = ctx.batch if total_tokens is None else int(total_tokens)
+    if token_offset % g or token_offset < 0 or token_offset + ctx.batch > total:
+        raise ValueError(f"token shard [{token_offset}, +{ctx.batch}) invalid for {total} tokens (block {g})")
     dev = dy.device
     transform = _lib.QT_TRANSFORM_RANDOMIZED if ctx.hadamard else _lib.QT_TRANSFORM_NONE
-    signs = sign_bits(xi, max(ctx.batch, ctx.d_out), dev) if ctx.hadamard else None
+    d_signs = sign_bits(xi, ctx.d_out, dev) if ctx.hadamard else None                       # along d_out
+    t_signs = sign_bits(xi, ctx.batch, dev, start=token_offset) if ctx.hadamard else None   # along tokens
     sr = rounding == "sr"
     err = _err_flag(dev) if check_finite else None
 
     # both dy operands from one read of dy: G (rows, qlinear.py:214) and G_t (cols, qlinear.py:234)
-    g_q, gt_q = quant_dual(dy, rc, transform=transform, signs=signs, prescale=PRE_SCALE,
+    g_q, gt_q = quant_dual(dy, rc, transform=transform, signs=d_signs, col_signs=t_signs, prescale=PRE_SCALE,
                            seed_rows=derive_seed(xi, _TAG_BWD_G1) if sr else 0,
-                           seed_cols=derive_seed(xi, _TAG_BWD_G2) if sr else 0, err=err)
+                           row_counter_start=token_offset * ctx.d_out,
+                           seed_cols=derive_seed(xi, _TAG_BWD_G2) if sr else 0,
+                           col_counter_start=token_offset, col_counter_ld=total, err=err)
 
     # input gradient: contract over d_out (qlinear.py:212-230)
-    wt_q = quant_cols(ctx.w_q, rc, transform=transform, signs=signs, prescale=PRE_SCALE,
+    wt_q = quant_cols(ctx.w_q, rc, transform=transform, signs=d_signs, prescale=PRE_SCALE,
                       sr_seed=derive_seed(xi, _TAG_BWD_W) if sr else 0, err=err)
     dx = gemm(g_q, wt_q, out_dtype=dx_dtype, mask=ctx.x_q.mask, hadamard=ctx.hadamard, scale=_POST_F32)
 
     # weight gradient: contract over batch (qlinear.py:232-250)
-    xt_q = quant_cols(ctx.x_q, rc, transform=transform, signs=signs, prescale=PRE_SCALE,
-                      sr_seed=derive_seed(xi, _TAG_BWD_X) if sr else 0, err=err)
+    xt_q = quant_cols(ctx.x_q, rc, transform=transform, signs=t_signs, prescale=PRE_SCALE,
+                      sr_seed=derive_seed(xi, _TAG_BWD_X) if sr else 0, counter_start=token_offset,
+                      counter_ld=total, err=err)
     dw = gemm(gt_q, xt_q, out_dtype=dw_dtype, mask=ctx.w_q.mask, hadamard=ctx.hadamard, scale=_POST_F32)
     _raise_if_nonfinite(err)
     if return_operands:
