@@ -96,11 +96,11 @@ QT_API int qt_fwht32(const float* x, float* out, int64_t rows, int64_t cols, int
  * qt_quant_rows: groups along the contiguous axis of x[rows, cols] (row stride ldx elements).
  *   transform (+ sign_bits for RANDOMIZED, indexed by column), then * prescale (1.0 or 0.75,
  *   qlinear.py:219-220), then quantize with `rounding` (SR: seed = per-tensor seed, stream
- *   position counter_start + r*cols + c, quantizers.py:79-84).
+ *   position counter_start + r*ld + c with ld = counter_ld or cols, quantizers.py:79-84).
  *   Replaces: kernels.fwht + kernels.quantize_{quest,rtn,sr} on a row-major matrix. */
 QT_API int qt_quant_rows(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_t cols, int transform,
                   const uint32_t* sign_bits, float prescale, int rounding, uint64_t sr_seed, uint64_t counter_start,
-                  uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, uint32_t* mask, int* err,
+                  int64_t counter_ld, uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, uint32_t* mask, int* err,
                   int* fallbacks, void* stream);
 
 /* qt_quant_cols: quantize the TRANSPOSE of x[rows, cols]: output operand [cols, rows] with groups

@@ -61,7 +61,7 @@ int qt_fwht32(const float* x, float* out, int64_t rows, int64_t cols, int transf
 
 int qt_quant_rows(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_t cols, int transform,
                   const uint32_t* sign_bits, float prescale, int rounding, uint64_t sr_seed, uint64_t counter_start,
-                  uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, uint32_t* mask, int* err, int* fallbacks,
+                  int64_t counter_ld, uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, uint32_t* mask, int* err, int* fallbacks,
                   void* stream) {
     if (cols % 32 != 0 || rows < 0) return QT_ERR_SHAPE;
     if (in_dtype != QT_IN_BF16 && in_dtype != QT_IN_F32) return QT_ERR_ARG;
@@ -69,7 +69,7 @@ int qt_quant_rows(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_
     if (transform == QT_TRANSFORM_RANDOMIZED && !sign_bits) return QT_ERR_ARG;
     int esz = in_dtype == QT_IN_BF16 ? 2 : 4;
     if (!al16(x) || (ldx * esz) % 16 || !al16(codes) || ldc % 16) return QT_ERR_ALIGN;
-    QuantCfg cfg{transform, sign_bits, prescale, rounding, sr_base_of(sr_seed), counter_start, 0};
+    QuantCfg cfg{transform, sign_bits, prescale, rounding, sr_base_of(sr_seed), counter_start, counter_ld};
     QuantOut out{codes, ldc, sf, katoms, mask, err, fallbacks};
     return launch_quant_rows(x, in_dtype, ldx, rows, cols, cfg, out, (cudaStream_t)stream);
 }
@@ -122,7 +122,7 @@ int qt_quant_dual(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_
 int qt_quant_fwd_quest(const void* x, int in_dtype, int64_t rows, int64_t cols, int hadamard, uint8_t* codes,
                        uint8_t* sf, uint32_t* mask, int* err, void* stream) {
     return qt_quant_rows(x, in_dtype, cols, rows, cols, hadamard ? QT_TRANSFORM_HADAMARD : QT_TRANSFORM_NONE, nullptr,
-                         1.0f, QT_ROUND_QUEST, 0, 0, codes, qt_codes_ld(cols), sf, qt_sf_katoms(cols), mask, err,
+                         1.0f, QT_ROUND_QUEST, 0, 0, 0, codes, qt_codes_ld(cols), sf, qt_sf_katoms(cols), mask, err,
                          nullptr, stream);
 }
 
@@ -130,7 +130,7 @@ int qt_quant_bwd_rows(const void* dy, int in_dtype, int64_t rows, int64_t cols, 
                       int rounding, uint64_t sr_seed, uint8_t* codes, uint8_t* sf, int* err, void* stream) {
     if (rounding == QT_ROUND_QUEST) return QT_ERR_ARG;
     return qt_quant_rows(dy, in_dtype, cols, rows, cols, sign_bits ? QT_TRANSFORM_RANDOMIZED : QT_TRANSFORM_NONE,
-                         sign_bits, 0.75f, rounding, sr_seed, 0, codes, qt_codes_ld(cols), sf, qt_sf_katoms(cols),
+                         sign_bits, 0.75f, rounding, sr_seed, 0, 0, codes, qt_codes_ld(cols), sf, qt_sf_katoms(cols),
                          nullptr, err, nullptr, stream);
 }
 

@@ -121,7 +121,8 @@ def fwht32(x: torch.Tensor, transform: int = 1, signs: torch.Tensor | None = Non
 
 
 def quant_rows(x: torch.Tensor, transform: int, rounding: int, *, signs: torch.Tensor | None = None,
-               prescale: float = 1.0, sr_seed: int = 0, counter_start: int = 0, want_mask: bool = False,
+               prescale: float = 1.0, sr_seed: int = 0, counter_start: int = 0, counter_ld: int = 0,
+               want_mask: bool = False,
                err: torch.Tensor | None = None, fallbacks: torch.Tensor | None = None,
                out: MXOperand | None = None) -> MXOperand:
     _require_cuda(x, "x")
@@ -136,7 +137,7 @@ def quant_rows(x: torch.Tensor, transform: int, rounding: int, *, signs: torch.T
     L = _lib.load()
     rc = L.qt_quant_rows(x.data_ptr(), _in_dtype(x), x.stride(0), rows, cols, transform,
                          signs.data_ptr() if signs is not None else None, float(prescale), rounding,
-                         int(sr_seed) & 0xFFFFFFFFFFFFFFFF, int(counter_start),
+                         int(sr_seed) & 0xFFFFFFFFFFFFFFFF, int(counter_start), int(counter_ld),
                          op.codes.data_ptr(), op.codes.stride(0), op.sf.data_ptr(), op.katoms,
                          op.mask.data_ptr() if op.mask is not None else None,
                          err.data_ptr() if err is not None else None,

@@ -55,7 +55,7 @@ def test_host_helpers(lib, oracle):
 
 def test_argument_errors_without_gpu(lib):
     # shape / enum validation happens before any CUDA call
-    assert lib.qt_quant_rows(None, 0, 33, 4, 33, 0, None, 1.0, 0, 0, 0, None, 16, None, 2, None, None, None,
+    assert lib.qt_quant_rows(None, 0, 33, 4, 33, 0, None, 1.0, 0, 0, 0, 0, None, 16, None, 2, None, None, None,
                              None) == 2001
     assert lib.qt_gemm_mxf4(None, None, None, None, 32, 32, 48, None, 0, 32, 0, None, 1.0, None) == 2001
     assert lib.qt_gemm_mxf4(None, None, None, None, 32, 32, 64, None, 7, 32, 0, None, 1.0, None) == 2003

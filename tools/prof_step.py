@@ -22,10 +22,23 @@ def main():
     ap.add_argument("--iters", type=int, default=2)
     ap.add_argument("--rounding", default="rtn")
     ap.add_argument("--events", action="store_true", help="print per-call CUDA-event times")
+    ap.add_argument("--all-shapes", action="store_true", help="the bench step: 4096->4096, 4096->11008, 11008->4096")
     a = ap.parse_args()
     qt.load()
     dev = torch.device("cuda")
     g = torch.Generator(device=dev).manual_seed(0)
+    if a.all_shapes:
+        data = []
+        for d_in, d_out in ((4096, 4096), (4096, 11008), (11008, 4096)):
+            data.append((torch.randn(a.tokens, d_in, device=dev, generator=g).to(torch.bfloat16),
+                         torch.randn(d_out, d_in, device=dev, generator=g) / d_in ** 0.5,
+                         torch.randn(a.tokens, d_out, device=dev, generator=g).to(torch.bfloat16)))
+        for it in range(a.iters):
+            for i, (x, w, dy) in enumerate(data):
+                y, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False)
+                qt.backward(dy, ctx, xi=it * 3 + i, rounding=a.rounding, dx_dtype=torch.bfloat16, check_finite=False)
+        torch.cuda.synchronize()
+        return
     x = torch.randn(a.tokens, a.din, device=dev, generator=g).to(torch.bfloat16)
     w = torch.randn(a.dout, a.din, device=dev, generator=g) / a.din ** 0.5
     dy = torch.randn(a.tokens, a.dout, device=dev, generator=g).to(torch.bfloat16)
