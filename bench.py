@@ -135,7 +135,7 @@ def kernel_table(qt, data, dev, reps=10):
     import torch
 
     from paper_2505_14669_b200 import _lib
-    from paper_2505_14669_b200.mxfp4 import gemm, quant_cols, quant_dual, quant_rows, sign_bits
+    from paper_2505_14669_b200.mxfp4 import gemm, quant_dual, quant_fused, sign_bits
 
     op = 0.5 + 1 / 32          # bytes per element of one MXFP4 operand (codes + E8M0 scales)
     RH, RT = _lib.QT_TRANSFORM_HADAMARD, _lib.QT_TRANSFORM_RANDOMIZED
@@ -155,23 +155,21 @@ def kernel_table(qt, data, dev, reps=10):
     for (x, w, dy) in data:
         T, d_in = x.shape
         d_out = w.shape[0]
-        _, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False)
-        signs = sign_bits(7, max(T, d_out), dev)
-        g_q, gt_q = quant_dual(dy, _lib.QT_ROUND_RTN, transform=RT, signs=signs, prescale=0.75)
-        wt_q = quant_cols(ctx.w_q, _lib.QT_ROUND_RTN, transform=RT, signs=signs, prescale=0.75)
-        xt_q = quant_cols(ctx.x_q, _lib.QT_ROUND_RTN, transform=RT, signs=signs, prescale=0.75)
+        _, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False, bwd_xi=7)
+        xt_q, wt_q = ctx.eager.xt_q, ctx.eager.wt_q
+        t_signs, d_signs = ctx.eager.t_signs, ctx.eager.d_signs
+        g_q, gt_q = quant_dual(dy, _lib.QT_ROUND_RTN, transform=RT, signs=d_signs, col_signs=t_signs, prescale=0.75)
         fl = 2.0 * T * d_in * d_out
+        QQ, RTN = _lib.QT_ROUND_QUEST, _lib.QT_ROUND_RTN
         cases = [
-            ("quant_fwd_x", lambda: quant_rows(x, RH, _lib.QT_ROUND_QUEST, want_mask=True),
-             T * d_in * (2 + op + 1 / 8), 0),
-            ("quant_fwd_w", lambda: quant_rows(w, RH, _lib.QT_ROUND_QUEST, want_mask=True),
-             d_out * d_in * (4 + op + 1 / 8), 0),
-            ("quant_dual_dy", lambda: quant_dual(dy, _lib.QT_ROUND_RTN, transform=RT, signs=signs, prescale=0.75),
+            # X -> X_q (+ trust mask) and X_t from one read of X; same for the fp32 master W
+            ("quant_fused_x", lambda: quant_fused(x, QQ, RTN, transform=RH, col_transform=RT, col_signs=t_signs),
+             T * d_in * (2 + 2 * op + 1 / 8), 0),
+            ("quant_fused_w", lambda: quant_fused(w, QQ, RTN, transform=RH, col_transform=RT, col_signs=d_signs),
+             d_out * d_in * (4 + 2 * op + 1 / 8), 0),
+            ("quant_dual_dy", lambda: quant_dual(dy, RTN, transform=RT, signs=d_signs, col_signs=t_signs,
+                                                 prescale=0.75),
              T * d_out * (2 + 2 * op), 0),
-            ("requant_wt", lambda: quant_cols(ctx.w_q, _lib.QT_ROUND_RTN, transform=RT, signs=signs, prescale=0.75),
-             d_out * d_in * 2 * op, 0),
-            ("requant_xt", lambda: quant_cols(ctx.x_q, _lib.QT_ROUND_RTN, transform=RT, signs=signs, prescale=0.75),
-             T * d_in * 2 * op, 0),
             ("gemm_fwd", lambda: gemm(ctx.x_q, ctx.w_q, out_dtype=torch.bfloat16), 0, fl),
             ("gemm_dx", lambda: gemm(g_q, wt_q, out_dtype=torch.bfloat16, mask=ctx.x_q.mask, scale=16 / 9), 0, fl),
             ("gemm_dw", lambda: gemm(gt_q, xt_q, out_dtype=torch.float32, mask=ctx.w_q.mask, scale=16 / 9), 0, fl),
@@ -208,7 +206,9 @@ def run_ours(args, rank, world, local_rank):
 
     def step(xi):
         for i, (x, w, dy) in enumerate(data):
-            y, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False)
+            # the step's backward seed is known at forward time (train.py:346-348), so X_t / W_t come
+            # out of the forward read of X / W (qt_quant_fused)
+            y, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False, bwd_xi=xi * 3 + i)
             dx, dw = qt.backward(dy, ctx, xi=xi * 3 + i, dx_dtype=torch.bfloat16, dw_dtype=torch.float32,
                                  check_finite=False)
             if world > 1:  # data parallel: the token-sum of dW is the only exchange (bf16, NCCL)
@@ -291,7 +291,7 @@ def run_ours(args, rank, world, local_rank):
             xd = hx.to(dev, non_blocking=True)
             dyd = hdy.to(dev, non_blocking=True)
             h2d += hx.numel() * 2 + hdy.numel() * 2
-            y, ctx = qt.forward(xd, w_dev, out_dtype=torch.bfloat16, check_finite=False)
+            y, ctx = qt.forward(xd, w_dev, out_dtype=torch.bfloat16, check_finite=False, bwd_xi=xi * 3 + i)
             dx, dw = qt.backward(dyd, ctx, xi=xi * 3 + i, dx_dtype=torch.bfloat16, check_finite=False)
             ox.copy_(dx, non_blocking=True)
             ow.copy_(dw, non_blocking=True)
@@ -357,8 +357,8 @@ def run_ours(args, rank, world, local_rank):
                                "share_of_step": round(q_us * 1e-3 / ms, 4)},
         "kernels": table,
         "e2e": e2e,
-        # per step and shape: 2 forward quantizers + 1 GEMM; 2 sign bitmaps + 1 dual + 2 requant + 2 GEMMs
-        "gpu_launches": 10 * len(SHAPES) * args.steps,
+        # per step and shape: 2 sign bitmaps + 2 fused forward quantizers + 1 GEMM; 1 dual quantizer + 2 GEMMs
+        "gpu_launches": 8 * len(SHAPES) * args.steps,
         "clocks": clocks,
     }
 

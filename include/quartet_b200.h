@@ -129,6 +129,22 @@ QT_API int qt_quant_dual(const void* x, int in_dtype, int64_t ldx, int64_t rows,
                          uint8_t* row_sf, int64_t row_katoms, uint32_t* row_mask, uint8_t* col_codes,
                          int64_t col_ldc, uint8_t* col_sf, int64_t col_katoms, int* err, void* stream);
 
+/* qt_quant_fused: a forward operand AND its transposed backward requantization from ONE read of x:
+ *   row operand [rows, cols] = Q_row(T_row(x) * row_prescale)        e.g. QuEST(H32(x)), qlinear.py:139-157
+ *   col operand [cols, rows] = Q_col(T_col(deq(row operand)^T) * col_prescale)
+ *                              == qt_requant_t of the row operand: X_t / W_t (qlinear.py:206-207, 215, 235)
+ * so the layer can produce X_t and W_t at forward time, when the backward seed xi is known (the training
+ * loop derives it per step and layer, train.py:346-348), instead of re-reading the saved operands.
+ * col_sign_bits are indexed by row (the contraction axis of the backward GEMM); col_rounding is RTN or SR
+ * (SR stream position col_counter_start + c*ld + r, ld = col_counter_ld or rows). */
+QT_API int qt_quant_fused(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_t cols, int row_transform,
+                          const uint32_t* row_sign_bits, float row_prescale, int row_rounding, uint64_t row_seed,
+                          uint64_t row_counter_start, int64_t row_counter_ld, uint8_t* row_codes, int64_t row_ldc,
+                          uint8_t* row_sf, int64_t row_katoms, uint32_t* row_mask, int col_transform,
+                          const uint32_t* col_sign_bits, float col_prescale, int col_rounding, uint64_t col_seed,
+                          uint64_t col_counter_start, int64_t col_counter_ld, uint8_t* col_codes, int64_t col_ldc,
+                          uint8_t* col_sf, int64_t col_katoms, int* err, int* fallbacks, void* stream);
+
 /* ---- named hot-path entry points (dense row-major inputs, ld == cols) ------------------- */
 
 /* Forward operand quantizer: x_h = H32(x) (if hadamard), QuEST -> codes/sf/mask.

@@ -38,6 +38,9 @@ SIGNATURES = {
                              _u64, _u64, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
     "qt_quant_dual": (_i32, [_vp, _i32, _i64, _i64, _i64, _i32, _vp, _vp, _f32, _i32, _u64, _u64, _u64, _u64,
                              _i64, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp]),
+    "qt_quant_fused": (_i32, [_vp, _i32, _i64, _i64, _i64, _i32, _vp, _f32, _i32, _u64, _u64, _i64, _vp, _i64, _vp,
+                              _i64, _vp, _i32, _vp, _f32, _i32, _u64, _u64, _i64, _vp, _i64, _vp, _i64, _vp, _vp,
+                              _vp]),
     "qt_quant_fwd_quest": (_i32, [_vp, _i32, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "qt_quant_bwd_rows": (_i32, [_vp, _i32, _i64, _i64, _vp, _i32, _u64, _vp, _vp, _vp, _vp]),
     "qt_quant_bwd_cols": (_i32, [_vp, _i32, _i64, _i64, _vp, _i32, _u64, _vp, _vp, _vp, _vp]),

@@ -93,7 +93,7 @@ int qt_quant_cols(const void* x, int in_dtype, int64_t ldx, const uint8_t* mx_co
     QuantCfg cfg{transform, sign_bits, prescale, rounding, sr_base_of(sr_seed), counter_start, counter_ld};
     QuantOut out{codes, ldc, sf, katoms, nullptr, err, nullptr};
     MxIn mx{mx_codes, mx_ldc, mx_sf, mx_katoms};
-    return launch_quant_tile(x, in_dtype, ldx, mx, rows, cols, nullptr, nullptr, &cfg, &out, (cudaStream_t)stream);
+    return launch_quant_tile(x, in_dtype, ldx, mx, rows, cols, nullptr, nullptr, &cfg, &out, 0, (cudaStream_t)stream);
 }
 
 int qt_quant_dual(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_t cols, int transform,
@@ -116,7 +116,34 @@ int qt_quant_dual(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_
     QuantOut ro{row_codes, row_ldc, row_sf, row_katoms, row_mask, err, nullptr};
     QuantOut co{col_codes, col_ldc, col_sf, col_katoms, nullptr, err, nullptr};
     MxIn mx{nullptr, 0, nullptr, 0};
-    return launch_quant_tile(x, in_dtype, ldx, mx, rows, cols, &rc, &ro, &cc, &co, (cudaStream_t)stream);
+    return launch_quant_tile(x, in_dtype, ldx, mx, rows, cols, &rc, &ro, &cc, &co, 0, (cudaStream_t)stream);
+}
+
+int qt_quant_fused(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_t cols, int row_transform,
+                   const uint32_t* row_sign_bits, float row_prescale, int row_rounding, uint64_t row_seed,
+                   uint64_t row_counter_start, int64_t row_counter_ld, uint8_t* row_codes, int64_t row_ldc,
+                   uint8_t* row_sf, int64_t row_katoms, uint32_t* row_mask, int col_transform,
+                   const uint32_t* col_sign_bits, float col_prescale, int col_rounding, uint64_t col_seed,
+                   uint64_t col_counter_start, int64_t col_counter_ld, uint8_t* col_codes, int64_t col_ldc,
+                   uint8_t* col_sf, int64_t col_katoms, int* err, int* fallbacks, void* stream) {
+    if (rows % 32 != 0 || cols % 32 != 0 || rows < 0) return QT_ERR_SHAPE;
+    if (in_dtype != QT_IN_BF16 && in_dtype != QT_IN_F32) return QT_ERR_ARG;
+    if (row_rounding < 0 || row_rounding > 2 || col_rounding < 1 || col_rounding > 2) return QT_ERR_ARG;
+    if (row_transform < 0 || row_transform > 2 || col_transform < 0 || col_transform > 2) return QT_ERR_ARG;
+    if ((row_transform == QT_TRANSFORM_RANDOMIZED && !row_sign_bits) ||
+        (col_transform == QT_TRANSFORM_RANDOMIZED && !col_sign_bits))
+        return QT_ERR_ARG;
+    int esz = in_dtype == QT_IN_BF16 ? 2 : 4;
+    if (!al16(x) || (ldx * esz) % 16 || !al16(row_codes) || row_ldc % 16 || !al16(col_codes) || col_ldc % 16)
+        return QT_ERR_ALIGN;
+    QuantCfg rc{row_transform, row_sign_bits, row_prescale, row_rounding, sr_base_of(row_seed), row_counter_start,
+                row_counter_ld};
+    QuantCfg cc{col_transform, col_sign_bits, col_prescale, col_rounding, sr_base_of(col_seed), col_counter_start,
+                col_counter_ld};
+    QuantOut ro{row_codes, row_ldc, row_sf, row_katoms, row_mask, err, fallbacks};
+    QuantOut co{col_codes, col_ldc, col_sf, col_katoms, nullptr, err, nullptr};
+    MxIn mx{nullptr, 0, nullptr, 0};
+    return launch_quant_tile(x, in_dtype, ldx, mx, rows, cols, &rc, &ro, &cc, &co, 1, (cudaStream_t)stream);
 }
 
 int qt_quant_fwd_quest(const void* x, int in_dtype, int64_t rows, int64_t cols, int hadamard, uint8_t* codes,

@@ -1,0 +1,220 @@
+// qgroup.cuh -- one 32-element MXFP4 group per call, scalar fp32 (the v3 quantizer pipeline).
+//
+// Bit-exact restatement of the reference transforms and quantizers (mx4train/_backend/_native.pyx):
+//   FWHT-32  fwht                 _native.pyx:353-379  stages h = 1..16, (a+b)*c / (a-b)*c, c = fp32(1/sqrt 2)
+//   RTN      quantize_rtn         _native.pyx:104-131
+//   SR       quantize_sr          _native.pyx:134-168  (sr_code in quant.cuh)
+//   QuEST    quantize_quest       _native.pyx:171-245  (fp32 search, exact f64 near-tie fallback)
+//
+// Why scalar: on B200 a packed FFMA2/FADD2 costs two issue cycles (measured, tools/ubench), so it moves
+// no more elements per clock than FFMA/FADD, while scalar code lets each thread hold ONE group (32
+// registers) and ptxas cannot contract __fmul_rn/__fadd_rn (it does contract mul.rn.f32x2 ->
+// add.rn.f32x2, see quant.cuh).  Every quantizer here is issue-bound, so the design counts issue slots:
+//   * bf16 inputs enter the first butterfly stage through FHADD.BF16 (add.rn.f32.bf16: one operand
+//     converted exactly inside the add), so the conversion of half the elements is free;
+//   * randomized-Hadamard signs are XORed onto whole bf16 words (one LOP3 per two elements) or folded
+//     into the dequantization scale (requantization of an MXFP4 operand);
+//   * the backward pre-scale 0.75 is folded into the power-of-two quantization scale when that is
+//     provably exact (e >= 4, see rtn_scale);
+//   * e2m1 bytes are packed with PRMT, -0 canonicalised with three LOP3/IADD per 8 nibbles.
+#pragma once
+#include "common.cuh"
+#include "quant.cuh"  // sr_code, quest_exact_cold (f64 reference search)
+
+namespace qt {
+
+constexpr float kHc = 0.70710678118654752440f;  // 0x3F3504F3 == (float)(1.0 / sqrt(2.0))
+
+// ------------------------------------------------------------------------- bf16 halves
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(__byte_perm(w, 0u, 0x1044)); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+// fp32 a +/- c where a is the low / high bf16 half of w (exact widening inside the add, one rounding).
+__device__ __forceinline__ float fh_add_lo(uint32_t w, float c) {
+    float d;
+    asm("{\n .reg .b16 l, h;\n mov.b32 {l, h}, %1;\n add.rn.f32.bf16 %0, l, %2;\n}" : "=f"(d) : "r"(w), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float fh_sub_lo(uint32_t w, float c) {
+    float d;
+    asm("{\n .reg .b16 l, h;\n mov.b32 {l, h}, %1;\n sub.rn.f32.bf16 %0, l, %2;\n}" : "=f"(d) : "r"(w), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float fh_add_hi(uint32_t w, float c) {
+    float d;
+    asm("{\n .reg .b16 l, h;\n mov.b32 {l, h}, %1;\n add.rn.f32.bf16 %0, h, %2;\n}" : "=f"(d) : "r"(w), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float fh_sub_hi(uint32_t w, float c) {
+    float d;
+    asm("{\n .reg .b16 l, h;\n mov.b32 {l, h}, %1;\n sub.rn.f32.bf16 %0, h, %2;\n}" : "=f"(d) : "r"(w), "f"(c));
+    return d;
+}
+
+// ------------------------------------------------------------------------------- FWHT-32
+__device__ __forceinline__ void bfly(float& a, float& b) {
+    const float s = __fadd_rn(a, b), d = __fsub_rn(a, b);
+    a = __fmul_rn(s, kHc);
+    b = __fmul_rn(d, kHc);
+}
+template <int H>
+__device__ __forceinline__ void fwht_stage1(float (&v)[32]) {
+#pragma unroll
+    for (int t = 0; t < 32; ++t)
+        if (!(t & H)) bfly(v[t], v[t + H]);
+}
+// stages h = 2..16 (stage 1 is done while loading)
+__device__ __forceinline__ void fwht_tail(float (&v)[32]) {
+    fwht_stage1<2>(v);
+    fwht_stage1<4>(v);
+    fwht_stage1<8>(v);
+    fwht_stage1<16>(v);
+}
+__device__ __forceinline__ void fwht_full(float (&v)[32]) {
+    fwht_stage1<1>(v);
+    fwht_tail(v);
+}
+
+// ------------------------------------------------------------------------------ absmax
+__device__ __forceinline__ float max3_nan(float a, float b, float c) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+// NaN-propagating max |v| (a NaN or Inf input shows up as a non-finite result)
+__device__ __forceinline__ float absmax32(const float (&v)[32]) {
+    float m0 = fabsf(v[0]), m1 = fabsf(v[1]);
+#pragma unroll
+    for (int j = 2; j < 30; j += 4) {
+        m0 = max3_nan(m0, fabsf(v[j]), fabsf(v[j + 1]));
+        m1 = max3_nan(m1, fabsf(v[j + 2]), fabsf(v[j + 3]));
+    }
+    return max3_nan(m0, fabsf(v[30]), max3_nan(m1, fabsf(v[31]), 0.0f));
+}
+
+// --------------------------------------------------------------------------- e2m1 pack
+__device__ __forceinline__ uint32_t e2m1b(float lo, float hi) {  // byte in bits 0..7, rest unspecified
+    uint32_t r;
+    asm("{\n .reg .b8 t;\n cvt.rn.satfinite.e2m1x2.f32 t, %2, %1;\n cvt.u32.u8 %0, t;\n}" : "=r"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+    return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+}
+// -0 (code 8) -> +0 on 8 nibbles: keep the sign only where the magnitude bits are non-zero
+__device__ __forceinline__ uint32_t canon8(uint32_t c) {
+    const uint32_t u = (c & 0x77777777u) + 0x77777777u;
+    return c & (u | 0x77777777u);
+}
+
+// RTN codes of v * sc (v * sc exact or rounded as the caller arranged), element 2k in the low nibble.
+__device__ __forceinline__ uint4 encode32(const float (&v)[32], float sc) {
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint32_t b[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) b[k] = e2m1b(__fmul_rn(v[8 * q + 2 * k], sc), __fmul_rn(v[8 * q + 2 * k + 1], sc));
+        w[q] = canon8(pack4(b[0], b[1], b[2], b[3]));
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+// Same plus the QuEST trust mask: bit j = |v_j * sc| <= 6 (6 - |a| is negative exactly when clipped).
+__device__ __forceinline__ uint4 encode32_mask(const float (&v)[32], float sc, uint32_t& keep) {
+    uint32_t w[4], clip = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint32_t b[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float a0 = __fmul_rn(v[8 * q + 2 * k], sc), a1 = __fmul_rn(v[8 * q + 2 * k + 1], sc);
+            b[k] = e2m1b(a0, a1);
+        }
+        w[q] = canon8(pack4(b[0], b[1], b[2], b[3]));
+    }
+#pragma unroll
+    for (int j = 31; j >= 0; --j) {
+        const float d = __fsub_rn(6.0f, fabsf(__fmul_rn(v[j], sc)));
+        clip = __funnelshift_l(__float_as_uint(d), clip, 1);
+    }
+    keep = ~clip;
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// ------------------------------------------------------------------------------- QuEST
+// Squared FP4 rounding error of v * sc (the error is sign-symmetric, so signed values round directly).
+__device__ __forceinline__ float quest_err32(const float (&v)[32], float sc) {
+    float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+        const float a = __fmul_rn(v[j], sc), b = __fmul_rn(v[j + 1], sc);
+        const float2 q = e2m1x2_to_f32(e2m1b(a, b));
+        const float ta = __fsub_rn(a, q.x), tb = __fsub_rn(b, q.y);
+        acc0 = __fmaf_rn(ta, ta, acc0);
+        acc1 = __fmaf_rn(tb, tb, acc1);
+    }
+    return __fadd_rn(acc0, acc1);
+}
+
+constexpr float kQTol = 6.103515625e-05f;        // 2^-14 relative near-tie guard
+constexpr float kQAtol = 7.52316384526264e-37f;  // 2^-120 absolute guard
+
+// QuEST scale exponent of one group with absmax `amax` (> 0, finite).  Candidates e_hi .. e_lo
+// (k = e_hi - e).  E_0 and E_1 always; k >= 2 only while the single-element clipping lower bound
+// (amax*sc_k - 6)^2 / sc_k^2, monotone in k, does not clear the best error by the guard -- so a
+// skipped candidate can never be the reference's choice.  Near-ties go to the exact f64 search.
+__device__ __forceinline__ int quest_search32(const float (&v)[32], float amax, int* fallback_counter) {
+    const int e_hi = ceil_scale_exp(amax), e_lo = quest_low_exp(amax);
+    if (e_hi <= e_lo) return e_hi;
+    const float sc0 = exp2i(127 - e_hi);
+    const float E0 = quest_err32(v, sc0);
+    const float E1 = __fmul_rn(quest_err32(v, __fmul_rn(sc0, 2.0f)), 0.25f);
+    float best = E0, second = E1;
+    int bk = 0;
+    if (E1 < E0) {
+        best = E1;
+        second = E0;
+        bk = 1;
+    }
+    const float a0 = __fmul_rn(amax, sc0);
+    for (int k = 2; k <= e_hi - e_lo; ++k) {
+        const float sk = exp2i(k), ik = exp2i(-2 * k);
+        const float d = __fsub_rn(__fmul_rn(a0, sk), 6.0f);
+        const float lb = __fmul_rn(__fmul_rn(d, d), ik);
+        if (__fmul_rn(lb, 0.99999905f) > __fadd_rn(__fmul_rn(best, 1.0f + kQTol), kQAtol)) break;
+        const float ek = __fmul_rn(quest_err32(v, __fmul_rn(sc0, sk)), ik);
+        if (ek < best) {
+            second = best;
+            best = ek;
+            bk = k;
+        } else if (ek < second) {
+            second = ek;
+        }
+    }
+    if (!(__fsub_rn(second, best) > __fadd_rn(__fmul_rn(second, kQTol), kQAtol))) {
+        if (fallback_counter) atomicAdd(fallback_counter, 1);
+        float xs[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) xs[j] = v[j];
+        return quest_exact_cold(xs, e_hi, e_lo);
+    }
+    return e_hi - bk;
+}
+
+// ---------------------------------------------------------------------- RTN scale rule
+// Quantization scale of a group whose values are y (FWHT output) and whose reference input is
+// fl(y * prescale): E8M0 e from fl(amax * prescale) (rounding is monotone, so that IS the absmax of the
+// pre-scaled values) and the multiplier prescale * 2^(127-e).  fl(y * (p * 2^k)) == fl(fl(y * p) * 2^k)
+// whenever neither product is subnormal; values whose scaled magnitude could reach a rounding
+// threshold (>= 0.25) are normal once e >= 4.  Below that the caller pre-scales explicitly.
+__device__ __forceinline__ bool rtn_scale(float amax, float prescale, int& e, float& sc) {
+    const float amp = prescale == 1.0f ? amax : __fmul_rn(amax, prescale);
+    e = ceil_scale_exp(amp);
+    if (prescale == 1.0f || e >= 4) {
+        sc = __fmul_rn(prescale, exp2i(127 - e));
+        return true;
+    }
+    sc = exp2i(127 - e);
+    return false;
+}
+
+}  // namespace qt

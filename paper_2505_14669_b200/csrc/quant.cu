@@ -1,18 +1,26 @@
-// quant.cu -- fused Hadamard + MXFP4 quantizer kernels (one HBM pass over the input).
+// quant.cu -- fused Hadamard + MXFP4 quantizer kernels (v3: scalar one-group pipeline, qgroup.cuh).
 //
 //   k_signs       sign bitmap of the randomized Hadamard (rng.py:57-62, hadamard.py:77-85)
-//   k_quant_tile  128 x 128 smem tile, up to two passes over the same data:
+//   k_quant       persistent tile kernel; per 128 x 128 tile (64 x 128 for fp32 input) up to two passes:
 //                   row pass  groups along the contiguous axis: forward X / W (H32 + QuEST,
-//                             qlinear.py:139-157) and the backward dy operand G (RHT32 + x0.75 +
-//                             RTN/SR, qlinear.py:214-225)
-//                   col pass  groups along the strided axis = the transposed operand
-//                             (dy^T -> G_t, deq(X_q)^T -> X_t, deq(W_q)^T -> W_t,
-//                              qlinear.py:215, 234-246)
-//                 so the backward's two dy operands come from ONE read of dy.  Every thread
-//                 quantizes two groups in lockstep (packed f32x2, see quant.cuh).
+//                             qlinear.py:139-157), the backward dy operand G (RHT32 + x0.75 + RTN/SR,
+//                             qlinear.py:214-225), or any quantize_{rtn,sr,quest} of the plugin seam
+//                   col pass  groups along the strided axis = the transposed operand, fed by
+//                             * the dense tile  (dy^T -> G_t, qlinear.py:234-245: one read of dy
+//                               gives both dy operands), or
+//                             * MXFP4 codes     deq(X_q)^T -> X_t and deq(W_q)^T -> W_t
+//                               (qlinear.py:206-207, 215, 235), either straight from the row pass of
+//                               the same tile (fused forward: X is read once for X_q AND X_t) or
+//                               from a saved operand in HBM (lazy requantization)
 //   k_transform_rows  transform only (the kernels.fwht seam)
+//
+// Thread mapping (256 threads):
+//   row pass  thread -> one tile row, 2 groups (processed one after the other; fp32 tiles: 1 group)
+//   col pass  thread -> column pair cp = t % 64 (groups A = column 2cp, B = 2cp+1), row group t / 64
+// Shared-memory layouts are XOR-swizzled so that the fill, both passes and the code exchange between
+// them are bank-conflict free (see tile_chunk / codes_chunk).
 #include "launch.h"
-#include "quant.cuh"
+#include "qgroup.cuh"
 
 namespace qt {
 
@@ -70,15 +78,11 @@ int launch_transform_rows(const float* x, float* out, int64_t rows, int64_t cols
     return (int)cudaGetLastError();
 }
 
-// ------------------------------------------------------------------------ k_quant_tile
-// Persistent kernel over 128 x 128 tiles.  Each CTA double-buffers tiles in dynamic smem with
-// cp.async (tile i+1 streams in while tile i is quantized), so HBM latency hides behind compute.
-// Dense tiles live in smem as bf16 (ESZ 2, 32 KB) or fp32 (ESZ 4, 64 KB) in 16-byte chunks; chunk
-// k of row r sits at k ^ sw(r, k), sw = 2 * ((r + r/32) & 3) ^ ((k / 8) & 1), which keeps (bf16) the
-// fill, the row pass (4 rows x 2 group pairs per phase) and the col pass (4 rows 32 apart x 2 chunks
-// per 32-lane load) bank-conflict free.  MXFP4 input is staged raw (codes + one 512-B scale atom)
-// and decoded exactly into a bf16 tile before the col pass.
-constexpr int kTR = 128, kTC = 128;
+// --------------------------------------------------------------------------------- k_quant
+enum RowMode : int { kRowOff = -1 };           // otherwise the rounding (kQuest / kRtn / kSr)
+enum ColSrc : int { kColOff = 0, kColDense = 1, kColCodes = 2 };
+
+constexpr int kTC = 128;  // tile columns (4 groups)
 
 struct TileArgs {
     const void* x;      // dense input (bf16 / fp32), row stride ldx elements
@@ -89,13 +93,31 @@ struct TileArgs {
     QuantOut row_out, col_out;
 };
 
-__device__ __forceinline__ int tile_chunk(int r, int k) { return k ^ ((((r + (r >> 5)) & 3) << 1) ^ ((k >> 3) & 1)); }
-
-// bf16x2 -> 2 x fp32 on the ALU pipe (PRMT + LOP3), keeping the FMA pipe free for the butterfly.
-__device__ __forceinline__ void bf16x2_to_f32(uint32_t w, float& lo, float& hi) {
-    lo = __uint_as_float(__byte_perm(w, 0u, 0x1044));
-    hi = __uint_as_float(w & 0xFFFF0000u);
+// dense tile: 16-byte chunk k of row r lives at chunk tile_chunk(r, k) of that row
+template <int ESZ>
+__device__ __forceinline__ int tile_chunk(int r, int k) {
+    if (ESZ == 2) return k ^ ((((r + (r >> 5)) & 3) << 1) ^ ((k >> 3) & 1));
+    return k ^ ((k >> 3) & 3) ^ ((r & 1) << 2);
 }
+// codes tile ([rows][64 B]): 16-byte chunk g (= group g of the row) at chunk g ^ ((r >> 1) & 1)
+__device__ __forceinline__ int codes_byte(int r, int b) { return r * 64 + (b ^ (((r >> 1) & 1) << 4)); }
+
+template <int IN>
+struct Geom {
+    static constexpr int ESZ = IN == kInF32 ? 4 : 2;
+    static constexpr int TR = IN == kInF32 ? 64 : 128;     // tile rows
+    static constexpr int CPR = kTC * ESZ / 16;              // dense chunks per row
+    static constexpr int DENSE = TR * CPR;                  // dense chunks per tile
+    static constexpr int RAW = TR * 4 + 512 / 16;           // MXFP4: code chunks + one scale atom
+    static constexpr int STAGE = IN == kInMXFP4 ? RAW : DENSE;
+    static constexpr int TSTRIDE = TR + 4;                  // floats per scale-table row (4 groups)
+    // smem: 2 input stages | codes tile (TR x 64 B) | scale table [4][TSTRIDE] f32 | row LUT [64] | col LUT [TR]
+    static constexpr int OFF_CODES = 2 * STAGE * 16;
+    static constexpr int OFF_T = OFF_CODES + TR * 64;
+    static constexpr int OFF_RLUT = OFF_T + 4 * TSTRIDE * 4;
+    static constexpr int OFF_CLUT = OFF_RLUT + 64 * 4;
+    static constexpr int BYTES = OFF_CLUT + TR * 4;
+};
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
@@ -106,33 +128,21 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 template <int IN>
-struct TileGeom {
-    static constexpr int ESZ = IN == kInF32 ? 4 : 2;
-    static constexpr int CPR = kTC * ESZ / 16;            // chunks per dense tile row
-    static constexpr int DENSE = kTR * CPR;               // chunks per dense tile
-    static constexpr int RAW_ROW = kTC / 2 / 16;          // MXFP4: code chunks per row (4)
-    static constexpr int RAW = kTR * RAW_ROW + 512 / 16;  // MXFP4: codes + one scale atom
-    // buffers: dense -> 2 x DENSE; MXFP4 -> 2 x RAW staging + 1 x DENSE decoded tile
-    static constexpr int CHUNKS = IN == kInMXFP4 ? 2 * RAW + DENSE : 2 * DENSE;
-    static constexpr int BYTES = CHUNKS * 16;
-};
-
-// Issue the cp.async copies of tile (r0, c0) into buffer `buf`.
-template <int IN>
-__device__ __forceinline__ void tile_fill_async(const TileArgs& a, uint4* buf, int64_t r0, int64_t c0, int tid) {
-    using G = TileGeom<IN>;
-    const int nr = (int)(a.R - r0 < kTR ? a.R - r0 : kTR), nc = (int)(a.C - c0 < kTC ? a.C - c0 : kTC);
+__device__ __forceinline__ void tile_fill_async(const TileArgs& a, uint8_t* buf, int64_t r0, int64_t c0, int tid) {
+    using G = Geom<IN>;
+    const int nr = (int)(a.R - r0 < G::TR ? a.R - r0 : G::TR), nc = (int)(a.C - c0 < kTC ? a.C - c0 : kTC);
+    uint4* b16 = reinterpret_cast<uint4*>(buf);
     if (IN == kInMXFP4) {
 #pragma unroll
-        for (int it = 0; it < kTR * G::RAW_ROW / 256; ++it) {
-            const int id = it * 256 + tid, rr = id / G::RAW_ROW, part = id % G::RAW_ROW;
+        for (int it = 0; it < G::TR * 4 / 256; ++it) {
+            const int id = it * 256 + tid, rr = id >> 2, part = id & 3;
             const bool ok = rr < nr && part * 32 < nc;
             const uint8_t* src = a.mx.codes + (ok ? (r0 + rr) * a.mx.ldc + c0 / 2 + part * 16 : 0);
-            cp_async16(buf + id, src, ok);
+            cp_async16(buf + codes_byte(rr, part * 16), src, ok);
         }
         if (tid < 32) {
             const uint8_t* src = a.mx.sf + ((r0 / 128) * a.mx.katoms + c0 / 128) * 512 + tid * 16;
-            cp_async16(buf + kTR * G::RAW_ROW + tid, src, true);
+            cp_async16(b16 + G::TR * 4 + tid, src, true);
         }
     } else {
         const uint8_t* xb = static_cast<const uint8_t*>(a.x);
@@ -141,192 +151,320 @@ __device__ __forceinline__ void tile_fill_async(const TileArgs& a, uint4* buf, i
             const int id = it * 256 + tid, rr = id / G::CPR, k = id % G::CPR;
             const bool ok = rr < nr && k * (16 / G::ESZ) < nc;
             const uint8_t* src = xb + (ok ? ((r0 + rr) * a.ldx + c0) * G::ESZ + k * 16 : 0);
-            cp_async16(buf + rr * G::CPR + tile_chunk(rr, k), src, ok);
+            cp_async16(b16 + rr * G::CPR + tile_chunk<G::ESZ>(rr, k), src, ok);
         }
     }
 }
 
-// MXFP4 staging -> decoded bf16 tile: thread (row t/2, groups 2h, 2h+1), exact code * 2^(e-127).
-__device__ __forceinline__ void tile_decode_mxfp4(const uint4* raw, uint4* tile, int tid) {
-    constexpr int CPR = kTC * 2 / 16;
-    const int rr = tid >> 1, h = tid & 1;
-    const uint8_t* sfa = reinterpret_cast<const uint8_t*>(raw + kTR * 4);
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-        const int gl = 2 * h + u;
-        const uint4 cw = raw[rr * 4 + gl];
-        const float s = exp2i((int)sfa[(rr & 31) * 16 + ((rr >> 5) & 3) * 4 + gl] - 127);
-        const uint32_t w[4] = {cw.x, cw.y, cw.z, cw.w};
+// ---------------------------------------------------------------------- group loaders
+// Row group g of tile row rr into v, with the transform's first butterfly stage fused into the load.
+template <int IN>
+__device__ __forceinline__ void load_row_group(const uint4* tile, int rr, int g, int transform, const uint32_t* rlut,
+                                               const uint32_t* sign_bits, int64_t gglob, float (&v)[32]) {
+    using G = Geom<IN>;
+    if (IN == kInBF16) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            uint32_t bw[4];
+            const uint4 c = tile[rr * G::CPR + tile_chunk<2>(rr, g * 4 + q)];
+            uint4 m = make_uint4(0, 0, 0, 0);
+            if (transform == kRandomized) m = reinterpret_cast<const uint4*>(rlut)[g * 4 + q];
+            const uint32_t w[4] = {c.x ^ m.x, c.y ^ m.y, c.z ^ m.z, c.w ^ m.w};
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                float2 f = e2m1x2_to_f32((w[q] >> (8 * b)) & 0xFFu);
-                bw[b] = (__float_as_uint(f.x * s) >> 16) | (__float_as_uint(f.y * s) & 0xFFFF0000u);
-            }
-            tile[rr * CPR + tile_chunk(rr, gl * 4 + q)] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
-        }
-    }
-}
-
-// Row pass on one tile: thread -> (row t/2, group pair t%2) = groups A = 2pp, B = 2pp + 1.
-template <int ESZ, int ROUND>
-__device__ __forceinline__ void tile_row_pass(const TileArgs& a, const uint4* tile, int64_t r0, int64_t c0, int nr,
-                                              int nc, int tid) {
-    constexpr int CPR = kTC * ESZ / 16;
-    const int rr = tid >> 1, pp = tid & 1;
-    const bool okA = rr < nr && 64 * pp < nc, okB = rr < nr && 64 * pp + 32 < nc;
-    Pair g;
-#pragma unroll
-    for (int hB = 0; hB < 2; ++hB) {
-        const int gl = 2 * pp + hB;
-        if (ESZ == 2) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint4 c = tile[rr * CPR + tile_chunk(rr, gl * 4 + q)];
-                const uint32_t w[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    float lo, hi;
-                    bf16x2_to_f32(w[t], lo, hi);
-                    if (hB) {
-                        g.p[q * 8 + 2 * t].y = lo;
-                        g.p[q * 8 + 2 * t + 1].y = hi;
-                    } else {
-                        g.p[q * 8 + 2 * t].x = lo;
-                        g.p[q * 8 + 2 * t + 1].x = hi;
-                    }
-                }
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const uint4 c = tile[rr * CPR + tile_chunk(rr, gl * 8 + q)];
-                const float v[4] = {__uint_as_float(c.x), __uint_as_float(c.y), __uint_as_float(c.z),
-                                    __uint_as_float(c.w)};
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    if (hB)
-                        g.p[q * 4 + t].y = v[t];
-                    else
-                        g.p[q * 4 + t].x = v[t];
+            for (int t = 0; t < 4; ++t) {
+                const int j = q * 8 + 2 * t;
+                if (transform != kNone) {
+                    const float hi = bf_hi(w[t]);
+                    v[j] = __fmul_rn(fh_add_lo(w[t], hi), kHc);
+                    v[j + 1] = __fmul_rn(fh_sub_lo(w[t], hi), kHc);
+                } else {
+                    v[j] = bf_lo(w[t]);
+                    v[j + 1] = bf_hi(w[t]);
                 }
             }
         }
-    }
-    const int64_t row = r0 + rr, gA = c0 / 32 + 2 * pp;
-    PairOut o;
-    o.sf[0] = o.sf[1] = 0;
-    if (okA) {
-        const QuantCfg& cf = a.row_cfg;
-        transform_pair(g, cf.transform, cf.transform == kRandomized ? __ldg(cf.sign_bits + gA) : 0u,
-                       cf.transform == kRandomized && okB ? __ldg(cf.sign_bits + gA + 1) : 0u, cf.prescale);
-        const int64_t cld = cf.counter_ld ? cf.counter_ld : a.C;
-        const uint64_t idx = cf.counter_start + (uint64_t)(row * cld + gA * 32);
-        o = quantize_pair<ROUND>(g, cf.sr_base, idx, idx + 32, a.row_out.err, a.row_out.fallbacks);
-        if (!okB) o.sf[1] = 0;
-        uint8_t* cp = a.row_out.codes + row * a.row_out.ldc + gA * 16;
-        *reinterpret_cast<uint4*>(cp) = o.codes[0];
-        if (okB) *reinterpret_cast<uint4*>(cp + 16) = o.codes[1];
-        if (a.row_out.mask) {
-            a.row_out.mask[row * (a.C / 32) + gA] = o.mask[0];
-            if (okB) a.row_out.mask[row * (a.C / 32) + gA + 1] = o.mask[1];
+        if (transform != kNone) fwht_tail(v);
+    } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint4 c = tile[rr * G::CPR + tile_chunk<4>(rr, g * 8 + q)];
+            v[4 * q] = __uint_as_float(c.x);
+            v[4 * q + 1] = __uint_as_float(c.y);
+            v[4 * q + 2] = __uint_as_float(c.z);
+            v[4 * q + 3] = __uint_as_float(c.w);
         }
-    }
-    // the 4 scale bytes of this tile row live in one atom word: combine the two lanes
-    const uint32_t mine = o.sf[0] | (o.sf[1] << 8);
-    const uint32_t other = __shfl_xor_sync(0xffffffffu, mine, 1);
-    if (pp == 0 && okA) {
-        uint8_t* sp = a.row_out.sf + sf_offset(row, c0 / 32, a.row_out.katoms);
-        const uint32_t w = mine | (other << 16);
-        if (nc == kTC)
-            *reinterpret_cast<uint32_t*>(sp) = w;
-        else
-            for (int j = 0; j * 32 < nc; ++j) sp[j] = (uint8_t)(w >> (8 * j));
+        if (transform == kRandomized) {
+            const uint32_t s = __ldg(sign_bits + gglob);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(__float_as_uint(v[j]) ^ ((s >> j) << 31));
+        }
+        if (transform != kNone) fwht_full(v);
     }
 }
 
-// Col pass on one tile: thread -> (column pair t/4, row group t%4): A = column 2cp, B = 2cp + 1.
-template <int ESZ, int ROUND>
-__device__ __forceinline__ void tile_col_pass(const TileArgs& a, const uint4* tile, int64_t r0, int64_t c0, int nr,
-                                              int nc, int tid) {
-    constexpr int CPR = kTC * ESZ / 16;
-    const int cp = tid >> 2, q = tid & 3;
-    const bool ok = 2 * cp < nc && q * 32 < nr;
-    Pair g;
-    // the swizzle of row q*32 + i depends on (i + q) & 3 only: 4 precomputed chunk offsets
-    const int kc = ESZ == 2 ? (cp >> 2) : (cp >> 1);
-    int off[4];
+// Column pair (columns 2cp, 2cp+1; tile rows q*32 .. q*32+31) of a dense tile into a / b.
+template <int IN>
+__device__ __forceinline__ void load_col_pair(const uint4* tile, int cp, int q, int transform, const uint32_t* clut,
+                                              float (&a)[32], float (&b)[32]) {
+    using G = Geom<IN>;
+    const int r0 = q * 32;
+    if (IN == kInBF16) {
+        const uint32_t* t32 = reinterpret_cast<const uint32_t*>(tile);
+        const int kc = cp >> 2, wd = cp & 3;
 #pragma unroll
-    for (int m = 0; m < 4; ++m) off[m] = tile_chunk(q * 32 + m, kc);
-    const uint4* base = tile + q * 32 * CPR;
+        for (int i = 0; i < 32; i += 2) {
+            const int r = r0 + i;
+            uint32_t w0 = t32[(r * G::CPR + tile_chunk<2>(r, kc)) * 4 + wd];
+            uint32_t w1 = t32[((r + 1) * G::CPR + tile_chunk<2>(r + 1, kc)) * 4 + wd];
+            if (transform == kRandomized) {
+                const uint2 m = *reinterpret_cast<const uint2*>(clut + r);
+                w0 ^= m.x;
+                w1 ^= m.y;
+            }
+            if (transform != kNone) {
+                const float nA = bf_lo(w1), nB = bf_hi(w1);
+                a[i] = __fmul_rn(fh_add_lo(w0, nA), kHc);
+                a[i + 1] = __fmul_rn(fh_sub_lo(w0, nA), kHc);
+                b[i] = __fmul_rn(fh_add_hi(w0, nB), kHc);
+                b[i + 1] = __fmul_rn(fh_sub_hi(w0, nB), kHc);
+            } else {
+                a[i] = bf_lo(w0);
+                b[i] = bf_hi(w0);
+                a[i + 1] = bf_lo(w1);
+                b[i + 1] = bf_hi(w1);
+            }
+        }
+        if (transform != kNone) {
+            fwht_tail(a);
+            fwht_tail(b);
+        }
+    } else {
+        const float2* t64 = reinterpret_cast<const float2*>(tile);
+        const int kc = cp >> 1, hf = cp & 1;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        const uint4* chunk = base + i * CPR + off[i & 3];
-        if (ESZ == 2) {
-            bf16x2_to_f32(reinterpret_cast<const uint32_t*>(chunk)[cp & 3], g.p[i].x, g.p[i].y);
+        for (int i = 0; i < 32; ++i) {
+            const int r = r0 + i;
+            float2 f = t64[(r * G::CPR + tile_chunk<4>(r, kc)) * 2 + hf];
+            if (transform == kRandomized) {
+                const uint32_t m = clut[r] & 0x80000000u;
+                f.x = __uint_as_float(__float_as_uint(f.x) ^ m);
+                f.y = __uint_as_float(__float_as_uint(f.y) ^ m);
+            }
+            a[i] = f.x;
+            b[i] = f.y;
+        }
+        if (transform != kNone) {
+            fwht_full(a);
+            fwht_full(b);
+        }
+    }
+}
+
+// Column pair from an MXFP4 codes tile: value = code * T[g][r] (T = +-2^(e-127), sign = RHT flip).
+__device__ __forceinline__ void load_col_codes(const uint8_t* codes, const float* T, int tstride, int cp, int q,
+                                               int transform, float (&a)[32], float (&b)[32]) {
+    const int g = cp >> 4;
+    const float4* trow = reinterpret_cast<const float4*>(T + g * tstride + q * 32);
+#pragma unroll
+    for (int i4 = 0; i4 < 8; ++i4) {
+        const float4 s = trow[i4];
+        const float sv[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = i4 * 4 + u, r = q * 32 + i;
+            const float2 f = e2m1x2_to_f32(codes[codes_byte(r, cp)]);
+            a[i] = __fmul_rn(f.x, sv[u]);
+            b[i] = __fmul_rn(f.y, sv[u]);
+        }
+    }
+    if (transform != kNone) {
+        fwht_full(a);
+        fwht_full(b);
+    }
+}
+
+// ------------------------------------------------------------------------ group quantizer
+// Quantize one transformed group v (pre-scale NOT yet applied).  Returns the E8M0 byte.
+template <int ROUND>
+__device__ __forceinline__ int quant_group(float (&v)[32], const QuantCfg& cf, uint64_t sr_idx, int* err,
+                                           int* fallbacks, uint4& codes, uint32_t& mask) {
+    const float am = absmax32(v);
+    if (!(am <= 3.4028234663852886e38f) && err) atomicOr(err, 1);
+    mask = 0xFFFFFFFFu;
+    int e;
+    if (ROUND == kQuest) {
+        if (cf.prescale != 1.0f) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], cf.prescale);
+        }
+        const float amp = cf.prescale != 1.0f ? __fmul_rn(am, cf.prescale) : am;
+        if (amp > 0.0f && amp <= 3.4028234663852886e38f) {
+            e = quest_search32(v, amp, fallbacks);
+            codes = encode32_mask(v, exp2i(127 - e), mask);
         } else {
-            g.p[i] = reinterpret_cast<const float2*>(chunk)[cp & 1];
+            e = 0;  // zero group: e = 0, codes 0, all kept (_native.pyx:228-233)
+            codes = make_uint4(0, 0, 0, 0);
         }
+    } else if (ROUND == kRtn) {
+        float sc;
+        if (!rtn_scale(am, cf.prescale, e, sc)) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], cf.prescale);
+        }
+        codes = encode32(v, sc);
+    } else {
+        if (cf.prescale != 1.0f) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], cf.prescale);
+        }
+        e = ceil_scale_exp(cf.prescale != 1.0f ? __fmul_rn(am, cf.prescale) : am);
+        const float sc_f = exp2i(127 - e);
+        const double sc_d = (double)sc_f;
+        uint32_t w[4];
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int j = qq * 8 + k;
+                acc |= sr_code(v[j], sc_f, sc_d, cf.sr_base, sr_idx + (uint64_t)j) << (4 * k);
+            }
+            w[qq] = acc;
+        }
+        codes = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    const int64_t orow = c0 + 2 * cp, ogrp = r0 / 32 + q;
-    PairOut o;
-    o.sf[0] = o.sf[1] = 0;
-    if (ok) {
-        const QuantCfg& cf = a.col_cfg;
-        const uint32_t s = cf.transform == kRandomized ? __ldg(cf.sign_bits + ogrp) : 0u;
-        transform_pair(g, cf.transform, s, s, cf.prescale);
-        const int64_t cld = cf.counter_ld ? cf.counter_ld : a.R;
-        const uint64_t idx = cf.counter_start + (uint64_t)(orow * cld + ogrp * 32);
-        o = quantize_pair<ROUND>(g, cf.sr_base, idx, idx + (uint64_t)cld, a.col_out.err, a.col_out.fallbacks);
-        *reinterpret_cast<uint4*>(a.col_out.codes + orow * a.col_out.ldc + ogrp * 16) = o.codes[0];
-        *reinterpret_cast<uint4*>(a.col_out.codes + (orow + 1) * a.col_out.ldc + ogrp * 16) = o.codes[1];
-    }
-    // gather the 4 scale bytes of each output row (lanes q = 0..3) into one atom word
-    uint32_t wA = o.sf[0] << (8 * q), wB = o.sf[1] << (8 * q);
-    wA |= __shfl_xor_sync(0xffffffffu, wA, 1);
-    wA |= __shfl_xor_sync(0xffffffffu, wA, 2);
-    wB |= __shfl_xor_sync(0xffffffffu, wB, 1);
-    wB |= __shfl_xor_sync(0xffffffffu, wB, 2);
-    if (2 * cp < nc && q < 2) {
-        const uint32_t w = q == 0 ? wA : wB;
-        uint8_t* sp = a.col_out.sf + sf_offset(orow + q, r0 / 32, a.col_out.katoms);
-        if (nr == kTR)
-            *reinterpret_cast<uint32_t*>(sp) = w;
-        else
-            for (int j = 0; j * 32 < nr; ++j) sp[j] = (uint8_t)(w >> (8 * j));
-    }
+    return e;
 }
 
-template <int IN, bool ROWS, bool COLS, int ROUND>
-__global__ void __launch_bounds__(256, IN == kInF32 ? 1 : 2) k_quant_tile(TileArgs a) {
-    using G = TileGeom<IN>;
-    extern __shared__ __align__(16) uint4 smem[];
+// ------------------------------------------------------------------------------- kernel
+template <int IN, int ROW, int COL, int CROUND>
+__global__ void __launch_bounds__(256, IN == kInF32 ? 1 : 2) k_quant(TileArgs a) {
+    using G = Geom<IN>;
+    constexpr int TR = G::TR;
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint8_t* codes_s = smem + G::OFF_CODES;
+    float* T = reinterpret_cast<float*>(smem + G::OFF_T);
+    uint32_t* rlut = reinterpret_cast<uint32_t*>(smem + G::OFF_RLUT);
+    uint32_t* clut = reinterpret_cast<uint32_t*>(smem + G::OFF_CLUT);
     const int tid = threadIdx.x;
-    const int64_t nRT = (a.R + kTR - 1) / kTR, nCT = (a.C + kTC - 1) / kTC, T = nRT * nCT;
-    constexpr int STAGE = IN == kInMXFP4 ? G::RAW : G::DENSE;
-    uint4* dec = smem + 2 * G::RAW;  // MXFP4 decoded tile
+    const int64_t nRT = (a.R + TR - 1) / TR, nCT = (a.C + kTC - 1) / kTC, NT = nRT * nCT;
+    const QuantCfg& rc = a.row_cfg;
+    const QuantCfg& cc = a.col_cfg;
 
     int64_t t = blockIdx.x;
-    if (t < T) tile_fill_async<IN>(a, smem, (t % nRT) * kTR, (t / nRT) * kTC, tid);
+    if (t < NT) tile_fill_async<IN>(a, smem, (t % nRT) * TR, (t / nRT) * kTC, tid);
     cp_async_commit();
-    for (int i = 0; t < T; ++i, t += gridDim.x) {
+    for (int it = 0; t < NT; ++it, t += gridDim.x) {
         const int64_t tn = t + gridDim.x;
-        if (tn < T) tile_fill_async<IN>(a, smem + ((i + 1) & 1) * STAGE, (tn % nRT) * kTR, (tn / nRT) * kTC, tid);
+        if (tn < NT) tile_fill_async<IN>(a, smem + ((it + 1) & 1) * G::STAGE * 16, (tn % nRT) * TR, (tn / nRT) * kTC, tid);
         cp_async_commit();
+        const int64_t r0 = (t % nRT) * TR, c0 = (t / nRT) * kTC;
+        const int nr = (int)(a.R - r0 < TR ? a.R - r0 : TR), nc = (int)(a.C - c0 < kTC ? a.C - c0 : kTC);
+        // per-tile sign LUTs: row pass (bf16 words along C), col pass (rows)
+        if (ROW != kRowOff && IN == kInBF16 && rc.transform == kRandomized && tid < 64) {
+            const int64_t col = c0 + 2 * tid;
+            uint32_t m = 0;
+            if (col < a.C) {
+                const uint32_t s = __ldg(rc.sign_bits + (col >> 5));
+                const int b = (int)(col & 31);
+                m = (((s >> b) & 1u) << 15) | (((s >> (b + 1)) & 1u) << 31);
+            }
+            rlut[tid] = m;
+        }
+        if (COL != kColOff && cc.transform == kRandomized && tid < TR) {
+            const int64_t row = r0 + tid;
+            uint32_t m = 0;
+            if (row < a.R) m = ((__ldg(cc.sign_bits + (row >> 5)) >> (row & 31)) & 1u) ? 0x80008000u : 0u;
+            clut[tid] = m;
+        }
         cp_async_wait1();
         __syncthreads();
-        const int64_t r0 = (t % nRT) * kTR, c0 = (t / nRT) * kTC;
-        const int nr = (int)(a.R - r0 < kTR ? a.R - r0 : kTR), nc = (int)(a.C - c0 < kTC ? a.C - c0 : kTC);
-        const uint4* tile = smem + (i & 1) * STAGE;
+        const uint8_t* stage = smem + (it & 1) * G::STAGE * 16;
+        const uint4* tile = reinterpret_cast<const uint4*>(stage);
+
         if (IN == kInMXFP4) {
-            tile_decode_mxfp4(tile, dec, tid);
+            // scale table of the staged operand: T[g][r] = (+-) 2^(e - 127)
+            const uint8_t* atom = stage + TR * 64;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int id = tid + 256 * u, r = id & 127, g = id >> 7;
+                const int e = atom[(r & 31) * 16 + ((r >> 5) & 3) * 4 + g];
+                float s = exp2i(e - 127);
+                if (cc.transform == kRandomized && (clut[r] & 1u << 31)) s = -s;
+                T[g * G::TSTRIDE + r] = s;
+            }
             __syncthreads();
-            tile = dec;
         }
-        if (ROWS) tile_row_pass<G::ESZ, ROUND>(a, tile, r0, c0, nr, nc, tid);
-        if (COLS) tile_col_pass<G::ESZ, ROUND>(a, tile, r0, c0, nr, nc, tid);
+
+        // ---------------------------------------------------------------- row pass
+        if (ROW != kRowOff) {
+            constexpr int GPT = TR == 128 ? 2 : 1;  // groups per thread
+            const int rr = TR == 128 ? tid >> 1 : tid >> 2;
+            const int64_t row = r0 + rr;
+            uint32_t sfw = 0;
+#pragma unroll
+            for (int h = 0; h < GPT; ++h) {
+                const int g = TR == 128 ? 2 * (tid & 1) + h : (tid & 3);
+                const bool ok = rr < nr && g * 32 < nc;
+                const int64_t gg = c0 / 32 + g;
+                int e = 0;
+                if (ok) {
+                    float v[32];
+                    load_row_group<IN>(tile, rr, g, rc.transform, rlut, rc.sign_bits, gg, v);
+                    const int64_t cld = rc.counter_ld ? rc.counter_ld : a.C;
+                    uint4 codes;
+                    uint32_t mask;
+                    e = quant_group<ROW>(v, rc, rc.counter_start + (uint64_t)(row * cld + gg * 32), a.row_out.err,
+                                         a.row_out.fallbacks, codes, mask);
+                    *reinterpret_cast<uint4*>(a.row_out.codes + row * a.row_out.ldc + gg * 16) = codes;
+                    if (a.row_out.mask) a.row_out.mask[row * (a.C / 32) + gg] = mask;
+                    if (COL == kColCodes) {
+                        *reinterpret_cast<uint4*>(codes_s + codes_byte(rr, g * 16)) = codes;
+                        float s = exp2i(e - 127);
+                        if (cc.transform == kRandomized && (clut[rr] & 1u << 31)) s = -s;
+                        T[g * G::TSTRIDE + rr] = s;
+                    }
+                }
+                sfw |= (uint32_t)e << (8 * g);
+            }
+            // the 4 scale bytes of this tile row form one atom word
+            if (TR == 128) {
+                sfw |= __shfl_xor_sync(0xffffffffu, sfw, 1);
+            } else {
+                sfw |= __shfl_xor_sync(0xffffffffu, sfw, 1);
+                sfw |= __shfl_xor_sync(0xffffffffu, sfw, 2);
+            }
+            if ((tid & (TR == 128 ? 1 : 3)) == 0 && rr < nr) {
+                uint8_t* sp = a.row_out.sf + sf_offset(row, c0 / 32, a.row_out.katoms);
+                if (nc == kTC)
+                    *reinterpret_cast<uint32_t*>(sp) = sfw;
+                else
+                    for (int j = 0; j * 32 < nc; ++j) sp[j] = (uint8_t)(sfw >> (8 * j));
+            }
+            if (COL == kColCodes) __syncthreads();
+        }
+
+        // ---------------------------------------------------------------- col pass
+        if (COL != kColOff) {
+            const int cp = tid & 63, q = tid >> 6;
+            if (q < TR / 32 && 2 * cp < nc && q * 32 < nr) {
+                float va[32], vb[32];
+                if (COL == kColDense)
+                    load_col_pair<IN>(tile, cp, q, cc.transform, clut, va, vb);
+                else
+                    load_col_codes(IN == kInMXFP4 ? stage : codes_s, T, G::TSTRIDE, cp, q, cc.transform, va, vb);
+                const int64_t orow = c0 + 2 * cp, ogrp = r0 / 32 + q;
+                const int64_t cld = cc.counter_ld ? cc.counter_ld : a.R;
+                const uint64_t idx = cc.counter_start + (uint64_t)(orow * cld + ogrp * 32);
+                uint4 codes;
+                uint32_t mask;
+                const int eA = quant_group<CROUND>(va, cc, idx, a.col_out.err, nullptr, codes, mask);
+                *reinterpret_cast<uint4*>(a.col_out.codes + orow * a.col_out.ldc + ogrp * 16) = codes;
+                const int eB = quant_group<CROUND>(vb, cc, idx + (uint64_t)cld, a.col_out.err, nullptr, codes, mask);
+                *reinterpret_cast<uint4*>(a.col_out.codes + (orow + 1) * a.col_out.ldc + ogrp * 16) = codes;
+                a.col_out.sf[sf_offset(orow, ogrp, a.col_out.katoms)] = (uint8_t)eA;
+                a.col_out.sf[sf_offset(orow + 1, ogrp, a.col_out.katoms)] = (uint8_t)eB;
+            }
+        }
         __syncthreads();
     }
 }
@@ -344,43 +482,65 @@ int launch_signs(uint32_t* bits, int64_t start, int64_t n, uint64_t xi, cudaStre
     return (int)cudaGetLastError();
 }
 
-template <int IN, bool ROWS, bool COLS, int ROUND>
-static void tile_launch(const TileArgs& a, dim3 grid, cudaStream_t st) {
-    constexpr int smem = TileGeom<IN>::BYTES;
+template <int IN, int ROW, int COL, int CROUND>
+static int quant_launch(const TileArgs& a, cudaStream_t st) {
+    using G = Geom<IN>;
+    auto fn = k_quant<IN, ROW, COL, CROUND>;
     static int ctas = 0;
     if (!ctas) {
-        auto fn = k_quant_tile<IN, ROWS, COLS, ROUND>;
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, G::BYTES);
         int dev = 0, sms = 148, per_sm = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, G::BYTES);
         ctas = sms * (per_sm > 0 ? per_sm : 1);
     }
-    const int64_t tiles = (int64_t)grid.x * grid.y;
+    const int64_t tiles = ((a.R + G::TR - 1) / G::TR) * ((a.C + kTC - 1) / kTC);
     const unsigned n = (unsigned)(tiles < ctas ? tiles : ctas);
-    k_quant_tile<IN, ROWS, COLS, ROUND><<<n, 256, smem, st>>>(a);
+    fn<<<n, 256, G::BYTES, st>>>(a);
+    return 0;
 }
 
-template <int IN, bool ROWS, bool COLS>
-static void tile_round_dispatch(const TileArgs& a, int round, dim3 grid, cudaStream_t st) {
-    if (round == kRtn)
-        tile_launch<IN, ROWS, COLS, kRtn>(a, grid, st);
-    else if (round == kSr)
-        tile_launch<IN, ROWS, COLS, kSr>(a, grid, st);
-    else
-        tile_launch<IN, ROWS, COLS, kQuest>(a, grid, st);
+template <int IN, int ROW, int COL>
+static int dispatch_cround(const TileArgs& a, int cround, cudaStream_t st) {
+    if (COL == kColOff) return quant_launch<IN, ROW, COL, kRtn>(a, st);
+    if (cround == kSr) return quant_launch<IN, ROW, COL, kSr>(a, st);
+    if (cround == kRtn) return quant_launch<IN, ROW, COL, kRtn>(a, st);
+    return 2003;
 }
 
-// Row and/or column passes over one read of x[R, C] (both passes share the rounding mode).
+template <int IN, int ROW>
+static int dispatch_col(const TileArgs& a, int col_src, int cround, cudaStream_t st) {
+    if (col_src == kColOff) return dispatch_cround<IN, ROW, kColOff>(a, cround, st);
+    if (col_src == kColCodes) {
+        if (ROW == kRowOff) return 2003;
+        return dispatch_cround<IN, ROW, kColCodes>(a, cround, st);
+    }
+    if (ROW == kQuest) return 2003;  // no dense col pass next to a QuEST row pass
+    return dispatch_cround<IN, ROW, kColDense>(a, cround, st);
+}
+
+template <int IN>
+static int dispatch_row(const TileArgs& a, int row, int col_src, int cround, cudaStream_t st) {
+    switch (row) {
+        case kRowOff: return dispatch_col<IN, kRowOff>(a, col_src, cround, st);
+        case kQuest: return dispatch_col<IN, kQuest>(a, col_src, cround, st);
+        case kRtn: return dispatch_col<IN, kRtn>(a, col_src, cround, st);
+        case kSr: return dispatch_col<IN, kSr>(a, col_src, cround, st);
+    }
+    return 2003;
+}
+
+// Row and/or column passes over one read of x[R, C].  col_from_codes: the col pass quantizes the
+// transpose of the row pass's dequantized result (fused forward) instead of the dense tile.
 int launch_quant_tile(const void* x, int in_type, int64_t ldx, const MxIn& mx, int64_t R, int64_t C,
                       const QuantCfg* row_cfg, const QuantOut* row_out, const QuantCfg* col_cfg,
-                      const QuantOut* col_out, cudaStream_t st) {
+                      const QuantOut* col_out, int col_from_codes, cudaStream_t st) {
     if (R == 0 || C == 0) return 0;
     const bool rows = row_cfg != nullptr, cols = col_cfg != nullptr;
     if (!rows && !cols) return 0;
-    if (rows && cols && row_cfg->rounding != col_cfg->rounding) return 2003;
     if (in_type == kInMXFP4 && rows) return 2003;  // MXFP4 input is only re-quantized transposed
+    if (cols && col_cfg->rounding == kQuest) return 2003;
     TileArgs a{};
     a.x = x;
     a.ldx = ldx;
@@ -395,32 +555,26 @@ int launch_quant_tile(const void* x, int in_type, int64_t ldx, const MxIn& mx, i
         a.col_cfg = *col_cfg;
         a.col_out = *col_out;
     }
-    const int round = rows ? row_cfg->rounding : col_cfg->rounding;
-    dim3 grid((unsigned)((R + kTR - 1) / kTR), (unsigned)((C + kTC - 1) / kTC));
+    const int row = rows ? row_cfg->rounding : (int)kRowOff;
+    const int col_src = !cols ? kColOff : (in_type == kInMXFP4 || col_from_codes) ? kColCodes : kColDense;
+    const int cround = cols ? col_cfg->rounding : kRtn;
+    int rc;
     if (in_type == kInMXFP4) {
-        tile_round_dispatch<kInMXFP4, false, true>(a, round, grid, st);
+        rc = cround == kSr ? quant_launch<kInMXFP4, kRowOff, kColCodes, kSr>(a, st)
+                           : quant_launch<kInMXFP4, kRowOff, kColCodes, kRtn>(a, st);
     } else if (in_type == kInBF16) {
-        if (rows && cols)
-            tile_round_dispatch<kInBF16, true, true>(a, round, grid, st);
-        else if (rows)
-            tile_round_dispatch<kInBF16, true, false>(a, round, grid, st);
-        else
-            tile_round_dispatch<kInBF16, false, true>(a, round, grid, st);
+        rc = dispatch_row<kInBF16>(a, row, col_src, cround, st);
     } else {
-        if (rows && cols)
-            tile_round_dispatch<kInF32, true, true>(a, round, grid, st);
-        else if (rows)
-            tile_round_dispatch<kInF32, true, false>(a, round, grid, st);
-        else
-            tile_round_dispatch<kInF32, false, true>(a, round, grid, st);
+        rc = dispatch_row<kInF32>(a, row, col_src, cround, st);
     }
+    if (rc) return rc;
     return (int)cudaGetLastError();
 }
 
 int launch_quant_rows(const void* x, int in_type, int64_t ldx, int64_t rows, int64_t cols, const QuantCfg& cfg,
                       const QuantOut& out, cudaStream_t st) {
     MxIn mx{nullptr, 0, nullptr, 0};
-    return launch_quant_tile(x, in_type, ldx, mx, rows, cols, &cfg, &out, nullptr, nullptr, st);
+    return launch_quant_tile(x, in_type, ldx, mx, rows, cols, &cfg, &out, nullptr, nullptr, 0, st);
 }
 
 }  // namespace qt

@@ -50,7 +50,10 @@ class MXOperand:
         if cols % GROUP:
             raise ValueError(f"axis length {cols} not divisible by block size {GROUP}")
         codes = torch.empty((rows, cols // 2), dtype=torch.uint8, device=device)
-        sf = torch.zeros(int(L.qt_sf_bytes(rows, cols)), dtype=torch.uint8, device=device)
+        # scale atoms: padding (rows to 256, groups to 8) must hold a finite exponent; without padding the
+        # quantizer writes every byte, so no fill kernel is needed
+        alloc = torch.empty if rows % 256 == 0 and cols % 256 == 0 else torch.zeros
+        sf = alloc(int(L.qt_sf_bytes(rows, cols)), dtype=torch.uint8, device=device)
         mask = torch.empty((rows, cols // GROUP), dtype=torch.int32, device=device) if with_mask else None
         return MXOperand(codes, sf, rows, cols, mask)
 
@@ -170,6 +173,35 @@ def quant_cols(x, rounding: int, *, transform: int, signs: torch.Tensor | None =
                          err.data_ptr() if err is not None else None, _stream(dev))
     check(rc, "qt_quant_cols")
     return op
+
+
+def quant_fused(x: torch.Tensor, rounding: int, col_rounding: int, *, transform: int, col_transform: int,
+                col_signs: torch.Tensor | None = None, prescale: float = 1.0, col_prescale: float = 0.75,
+                sr_seed: int = 0, col_seed: int = 0, col_counter_start: int = 0, col_counter_ld: int = 0,
+                want_mask: bool = True, err: torch.Tensor | None = None, fallbacks: torch.Tensor | None = None):
+    """A forward operand and its transposed backward requantization from ONE read of x[rows, cols]
+    (qt_quant_fused): returns (row operand [rows, cols] = Q(T(x)), col operand [cols, rows] =
+    Q_col(T_col(deq(row operand)^T) * col_prescale)), i.e. (X_q, X_t) or (W_q, W_t) of qlinear.py:139-157
+    and 206-207 / 215 / 235.  `col_signs` flips the row axis (the backward contraction axis)."""
+    _require_cuda(x, "x")
+    if x.stride(1) != 1:
+        x = x.contiguous()
+    rows, cols = x.shape
+    if rows % GROUP or cols % GROUP:
+        raise ValueError(f"fused quantization needs both axes divisible by {GROUP}: {rows}x{cols}")
+    r_op = MXOperand.empty(rows, cols, x.device, with_mask=want_mask)
+    c_op = MXOperand.empty(cols, rows, x.device)
+    rc = _lib.load().qt_quant_fused(x.data_ptr(), _in_dtype(x), x.stride(0), rows, cols, transform, None,
+                                    float(prescale), rounding, int(sr_seed) & 0xFFFFFFFFFFFFFFFF, 0, 0,
+                                    r_op.codes.data_ptr(), r_op.codes.stride(0), r_op.sf.data_ptr(), r_op.katoms,
+                                    r_op.mask.data_ptr() if r_op.mask is not None else None, col_transform,
+                                    col_signs.data_ptr() if col_signs is not None else None, float(col_prescale),
+                                    col_rounding, int(col_seed) & 0xFFFFFFFFFFFFFFFF, int(col_counter_start),
+                                    int(col_counter_ld), c_op.codes.data_ptr(), c_op.codes.stride(0), c_op.sf.data_ptr(),
+                                    c_op.katoms, err.data_ptr() if err is not None else None,
+                                    fallbacks.data_ptr() if fallbacks is not None else None, _stream(x.device))
+    check(rc, "qt_quant_fused")
+    return r_op, c_op
 
 
 def quant_dual(x: torch.Tensor, rounding: int, *, transform: int, signs: torch.Tensor | None = None,

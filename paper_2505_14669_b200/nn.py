@@ -28,9 +28,13 @@ class QuartetLinearFn(torch.autograd.Function):
         x2 = x.reshape(-1, x.shape[-1])
         if x2.dtype not in (torch.bfloat16, torch.float32):
             x2 = x2.float()
+        from .dp import ShardContext
+
+        # xi is known now, so X_t / W_t come out of the same read of x / w (qt_quant_fused)
         y, lctx = qlinear.forward(x2, w.detach(), scheme=scheme, hadamard=hadamard, seed=xi,
                                   out_dtype=x.dtype if x.dtype in (torch.bfloat16, torch.float32) else torch.float32,
-                                  check_finite=False)
+                                  check_finite=False, bwd_xi=int(xi), bwd_rounding=rounding,
+                                  token_offset=ShardContext.offset, total_tokens=ShardContext.total)
         ctx.lctx = lctx
         ctx.xi = int(xi)
         ctx.rounding = rounding

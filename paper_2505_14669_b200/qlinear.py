@@ -28,7 +28,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from .mxfp4 import GROUP, MXOperand, derive_seed, gemm, quant_cols, quant_dual, quant_rows, sign_bits
+from .mxfp4 import GROUP, MXOperand, derive_seed, gemm, quant_cols, quant_dual, quant_fused, quant_rows, sign_bits
 
 PRE_SCALE = 0.75                     # qlinear.py:36
 POST_SCALE = 16.0 / 9.0              # qlinear.py:37
@@ -98,6 +98,9 @@ class LayerContext:
     d_in: int
     d_out: int
 
+    # transposed backward operands built at forward time (forward(..., bwd_xi=...)); see _Eager
+    eager: "_Eager | None" = None
+
     @property
     def m_x(self) -> torch.Tensor:
         return self.x_q.mask_bool()
@@ -105,6 +108,24 @@ class LayerContext:
     @property
     def m_w(self) -> torch.Tensor:
         return self.w_q.mask_bool()
+
+
+@dataclass
+class _Eager:
+    """X_t, W_t and the sign bitmaps of backward(xi) quantized during forward (qt_quant_fused).
+
+    They are exactly what backward would compute from the saved X_q / W_q (qlinear.py:206-207, 215, 235),
+    so backward uses them when called with the same xi, rounding and token shard, and recomputes
+    them otherwise."""
+
+    xi: int
+    rounding: str
+    token_offset: int
+    total: int
+    xt_q: MXOperand
+    wt_q: MXOperand
+    d_signs: torch.Tensor | None
+    t_signs: torch.Tensor | None
 
 
 def _check_policy(policy: GemmPolicy, scheme: QuantScheme) -> None:
@@ -142,8 +163,15 @@ def quantize_operand(m: torch.Tensor, scheme: QuantScheme, hadamard: bool, seed:
 
 def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, policy: GemmPolicy = DEFAULT_POLICY,
             hadamard: bool = True, seed: int | None = None, out_dtype: torch.dtype = torch.float32,
-            check_finite: bool = True):
-    """y = x @ w.T through the quantized pipeline; returns (y, context)  (qlinear.py:114-165)."""
+            check_finite: bool = True, bwd_xi: int | None = None, bwd_rounding: str = "rtn", token_offset: int = 0,
+            total_tokens: int | None = None):
+    """y = x @ w.T through the quantized pipeline; returns (y, context)  (qlinear.py:114-165).
+
+    B200 extension: when the backward seed is already known (the training loop derives it per step and
+    layer, train.py:346-348), pass it as ``bwd_xi`` (with the backward ``bwd_rounding`` and, for a
+    data-parallel token shard, ``token_offset`` / ``total_tokens``): the same single read of x (and of w)
+    then also produces the transposed backward operands X_t and W_t (qt_quant_fused), which backward
+    reuses instead of re-reading X_q / W_q.  Results are identical either way."""
     _check_policy(policy, scheme)
     if x.dim() != 2 or w.dim() != 2:
         raise ValueError("x and w must be 2-D")
@@ -161,12 +189,33 @@ def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, polic
         sx = derive_seed(seed, _TAG_FWD_X)
         sw = derive_seed(seed, _TAG_FWD_W)
     err = _err_flag(x.device) if check_finite else None
-    x_q = quantize_operand(x, scheme, hadamard, sx, err)
-    w_q = quantize_operand(w, scheme, hadamard, sw, err)
+    eager = None
+    if bwd_xi is not None and bwd_rounding in ("rtn", "sr") and batch % g == 0 and d_out % g == 0:
+        total = batch if total_tokens is None else int(total_tokens)
+        if token_offset % g or token_offset < 0 or token_offset + batch > total:
+            raise ValueError(f"token shard [{token_offset}, +{batch}) invalid for {total} tokens (block {g})")
+        rc = _rounding_code(bwd_rounding)
+        sr = bwd_rounding == "sr"
+        row_rc = {"quest": _lib.QT_ROUND_QUEST, "rtn_absmax": _lib.QT_ROUND_RTN, "sr_absmax": _lib.QT_ROUND_SR}[scheme.kind]
+        fwd_t = _lib.QT_TRANSFORM_HADAMARD if hadamard else _lib.QT_TRANSFORM_NONE
+        bwd_t = _lib.QT_TRANSFORM_RANDOMIZED if hadamard else _lib.QT_TRANSFORM_NONE
+        d_signs = sign_bits(bwd_xi, d_out, x.device) if hadamard else None
+        t_signs = sign_bits(bwd_xi, batch, x.device, start=token_offset) if hadamard else None
+        x_q, xt_q = quant_fused(x, row_rc, rc, transform=fwd_t, col_transform=bwd_t, col_signs=t_signs,
+                                col_prescale=PRE_SCALE, sr_seed=sx or 0,
+                                col_seed=derive_seed(bwd_xi, _TAG_BWD_X) if sr else 0,
+                                col_counter_start=token_offset, col_counter_ld=total, err=err)
+        w_q, wt_q = quant_fused(w, row_rc, rc, transform=fwd_t, col_transform=bwd_t, col_signs=d_signs,
+                                col_prescale=PRE_SCALE, sr_seed=sw or 0,
+                                col_seed=derive_seed(bwd_xi, _TAG_BWD_W) if sr else 0, err=err)
+        eager = _Eager(int(bwd_xi), bwd_rounding, int(token_offset), total, xt_q, wt_q, d_signs, t_signs)
+    else:
+        x_q = quantize_operand(x, scheme, hadamard, sx, err)
+        w_q = quantize_operand(w, scheme, hadamard, sw, err)
     y = gemm(x_q, w_q, out_dtype=out_dtype)
     _raise_if_nonfinite(err)
     ctx = LayerContext(x_q=x_q, w_q=w_q, scheme=scheme, policy=policy, hadamard=hadamard,
-                       batch=batch, d_in=d_in, d_out=d_out)
+                       batch=batch, d_in=d_in, d_out=d_out, eager=eager)
     return y, ctx
 
 
@@ -207,8 +256,14 @@ def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn"
         raise ValueError(f"token shard [{token_offset}, +{ctx.batch}) invalid for {total} tokens (block {g})")
     dev = dy.device
     transform = _lib.QT_TRANSFORM_RANDOMIZED if ctx.hadamard else _lib.QT_TRANSFORM_NONE
-    d_signs = sign_bits(xi, ctx.d_out, dev) if ctx.hadamard else None                       # along d_out
-    t_signs = sign_bits(xi, ctx.batch, dev, start=token_offset) if ctx.hadamard else None   # along tokens
+    ea = ctx.eager
+    if ea is not None and (ea.xi, ea.rounding, ea.token_offset, ea.total) != (int(xi), rounding, token_offset, total):
+        ea = None
+    if ea is not None:
+        d_signs, t_signs = ea.d_signs, ea.t_signs
+    else:
+        d_signs = sign_bits(xi, ctx.d_out, dev) if ctx.hadamard else None                       # along d_out
+        t_signs = sign_bits(xi, ctx.batch, dev, start=token_offset) if ctx.hadamard else None   # along tokens
     sr = rounding == "sr"
     err = _err_flag(dev) if check_finite else None
 
@@ -220,14 +275,16 @@ def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn"
                            col_counter_start=token_offset, col_counter_ld=total, err=err)
 
     # input gradient: contract over d_out (qlinear.py:212-230)
-    wt_q = quant_cols(ctx.w_q, rc, transform=transform, signs=d_signs, prescale=PRE_SCALE,
-                      sr_seed=derive_seed(xi, _TAG_BWD_W) if sr else 0, err=err)
+    wt_q = ea.wt_q if ea is not None else quant_cols(ctx.w_q, rc, transform=transform, signs=d_signs,
+                                                     prescale=PRE_SCALE,
+                                                     sr_seed=derive_seed(xi, _TAG_BWD_W) if sr else 0, err=err)
     dx = gemm(g_q, wt_q, out_dtype=dx_dtype, mask=ctx.x_q.mask, hadamard=ctx.hadamard, scale=_POST_F32)
 
     # weight gradient: contract over batch (qlinear.py:232-250)
-    xt_q = quant_cols(ctx.x_q, rc, transform=transform, signs=t_signs, prescale=PRE_SCALE,
-                      sr_seed=derive_seed(xi, _TAG_BWD_X) if sr else 0, counter_start=token_offset,
-                      counter_ld=total, err=err)
+    xt_q = ea.xt_q if ea is not None else quant_cols(ctx.x_q, rc, transform=transform, signs=t_signs,
+                                                     prescale=PRE_SCALE,
+                                                     sr_seed=derive_seed(xi, _TAG_BWD_X) if sr else 0,
+                                                     counter_start=token_offset, counter_ld=total, err=err)
     dw = gemm(gt_q, xt_q, out_dtype=dw_dtype, mask=ctx.w_q.mask, hadamard=ctx.hadamard, scale=_POST_F32)
     _raise_if_nonfinite(err)
     if return_operands:

@@ -30,12 +30,16 @@ def _scheme(qt, kind):
     return {"quest": qt.QUEST, "rtn_absmax": qt.RTN_ABSMAX, "sr_absmax": qt.SR_ABSMAX}[kind]
 
 
+@pytest.mark.parametrize("eager", [False, True], ids=["lazy", "eager"])
 @pytest.mark.parametrize("case", ["quest_rtn", "quest_sr", "quest_rtn_t256", "rtnfwd_rtn", "quest_rtn_noh"])
-def test_golden_end_to_end(qt, oracle, case):
+def test_golden_end_to_end(qt, oracle, case, eager):
+    """eager: forward(..., bwd_xi=xi) builds X_t / W_t in the forward read (qt_quant_fused)."""
     z = np.load(os.path.join(GOLDEN, f"qlinear_{case}.npz"))
     had = bool(z["hadamard"])
+    kw = dict(bwd_xi=int(z["xi"]), bwd_rounding=str(z["rounding"])) if eager else {}
     y, ctx = qt.forward(to_dev(z["x"], torch.bfloat16), to_dev(z["w"], torch.bfloat16),
-                        scheme=_scheme(qt, str(z["scheme"])), hadamard=had)
+                        scheme=_scheme(qt, str(z["scheme"])), hadamard=had, **kw)
+    assert (ctx.eager is not None) == eager
     # saved context: bit-exact against the reference's LayerContext
     assert np.array_equal(ctx.x_q.codes.cpu().numpy(), z["x_codes"])
     assert np.array_equal(ctx.x_q.scales_rowmajor().cpu().numpy(), z["x_scales"])
@@ -56,8 +60,9 @@ def test_golden_end_to_end(qt, oracle, case):
         assert_operand_equal(ops[name], c, s, name)
 
 
+@pytest.mark.parametrize("eager", [False, True], ids=["lazy", "eager"])
 @pytest.mark.parametrize("rounding", ["rtn", "sr"])
-def test_config1_against_oracle(qt, oracle, rounding):
+def test_config1_against_oracle(qt, oracle, rounding, eager):
     """BASELINE config 1: 1024x1024 weight, 2048 tokens, g = 32 (the CPU reference's own case)."""
     T, d_in, d_out, xi = 2048, 1024, 1024, 7
     x = bf16_values(oracle.gaussians(1, oracle.DOMAIN_GAUSS, 0, T * d_in).reshape(T, d_in).astype(np.float32))
@@ -70,7 +75,9 @@ def test_config1_against_oracle(qt, oracle, rounding):
         dx_ref, dw_ref = oracle.backward(dy, octx, xi=xi, rounding=rounding)
     finally:
         oracle.set_threads(1)
-    y, ctx = qt.forward(to_dev(x, torch.bfloat16), to_dev(w, torch.bfloat16))
+    kw = dict(bwd_xi=xi, bwd_rounding=rounding) if eager else {}
+    y, ctx = qt.forward(to_dev(x, torch.bfloat16), to_dev(w, torch.bfloat16), **kw)
+    assert (ctx.eager is not None) == eager
     assert_operand_equal(ctx.x_q, octx.x_codes, octx.x_scales, "X_q")
     assert_operand_equal(ctx.w_q, octx.w_codes, octx.w_scales, "W_q")
     assert np.array_equal(ctx.m_x.cpu().numpy(), octx.m_x)

@@ -230,3 +230,33 @@ def test_fwht32_bit_exact(qt, oracle, prescale):
     ref = oracle.fwht(x * oracle.signs(5, 0, 256), 32) * np.float32(prescale)
     bad = np.argwhere(got.view(np.uint32) != ref.view(np.uint32))
     assert bad.size == 0, (len(bad), bad[:3], got[tuple(bad[0])], ref[tuple(bad[0])])
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("shape", [(96, 160), (320, 96), (256, 384)])
+@pytest.mark.parametrize("col_round", ["rtn", "sr"])
+@pytest.mark.parametrize("row_round", ["quest", "rtn"])
+def test_fused_forward_equals_rows_then_requant(qt, shape, dtype, col_round, row_round):
+    """qt_quant_fused (one read of x) == qt_quant_rows followed by qt_quant_cols on the saved operand,
+    including partial tiles (rows / cols not multiples of the 128 / 64-row tile)."""
+    from paper_2505_14669_b200 import _lib
+    from paper_2505_14669_b200.mxfp4 import quant_cols, quant_fused, quant_rows, sign_bits
+
+    g = torch.Generator(device="cuda").manual_seed(shape[0] + shape[1])
+    x = (torch.randn(*shape, device="cuda", generator=g) * 3).to(dtype)
+    x[5, :32] = 0  # a zero group
+    rr = {"quest": _lib.QT_ROUND_QUEST, "rtn": _lib.QT_ROUND_RTN}[row_round]
+    cr = {"rtn": _lib.QT_ROUND_RTN, "sr": _lib.QT_ROUND_SR}[col_round]
+    signs = sign_bits(11, shape[0], "cuda", start=64)
+    ref_row = quant_rows(x, _lib.QT_TRANSFORM_HADAMARD, rr, want_mask=True)
+    ref_col = quant_cols(ref_row, cr, transform=_lib.QT_TRANSFORM_RANDOMIZED, signs=signs, prescale=0.75,
+                         sr_seed=99, counter_start=64, counter_ld=shape[0] + 64)
+    row, col = quant_fused(x, rr, cr, transform=_lib.QT_TRANSFORM_HADAMARD,
+                           col_transform=_lib.QT_TRANSFORM_RANDOMIZED, col_signs=signs, col_prescale=0.75,
+                           col_seed=99, col_counter_start=64, col_counter_ld=shape[0] + 64)
+    torch.cuda.synchronize()
+    assert torch.equal(row.codes, ref_row.codes)
+    assert torch.equal(row.scales_rowmajor(), ref_row.scales_rowmajor())
+    assert torch.equal(row.mask, ref_row.mask)
+    assert torch.equal(col.codes, ref_col.codes)
+    assert torch.equal(col.scales_rowmajor(), ref_col.scales_rowmajor())

@@ -35,7 +35,8 @@ def main():
                          torch.randn(a.tokens, d_out, device=dev, generator=g).to(torch.bfloat16)))
         for it in range(a.iters):
             for i, (x, w, dy) in enumerate(data):
-                y, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False)
+                y, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False, bwd_xi=it * 3 + i,
+                                    bwd_rounding=a.rounding)
                 qt.backward(dy, ctx, xi=it * 3 + i, rounding=a.rounding, dx_dtype=torch.bfloat16, check_finite=False)
         torch.cuda.synchronize()
         return
@@ -65,7 +66,7 @@ def main():
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         s0.record()
-        y, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False)
+        y, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False, bwd_xi=it, bwd_rounding=a.rounding)
         dx, dw = qt.backward(dy, ctx, xi=it, rounding=a.rounding, dx_dtype=torch.bfloat16, check_finite=False)
         t1 = time.perf_counter()
         e0.record()
