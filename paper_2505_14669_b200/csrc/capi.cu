@@ -10,10 +10,18 @@ static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) 
 static inline uint64_t sr_base_of(uint64_t seed) { return mix64(seed ^ mix64(kDomainSR)); }
 
 static int g_gemm_dbg = 0;  // experiment knobs for qt_debug_set_gemm (never set in production)
+static int g_quant_mode = 0;          // qt_debug_set_quant: 0 auto (tensor-core path when eligible), 1 CUDA cores
+static int* g_quant_fallbacks = nullptr;
 
 extern "C" {
 
 void qt_debug_set_gemm(int dbg) { g_gemm_dbg = dbg; }
+
+void qt_debug_set_quant(int mode, int* fallbacks) {
+    qt::g_tcq_dbg = mode >> 4;
+    g_quant_mode = mode & 15;
+    g_quant_fallbacks = fallbacks;
+}
 
 int qt_abi_version(void) { return QT_ABI_VERSION; }
 
@@ -115,6 +123,13 @@ int qt_quant_dual(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_
                 col_counter_ld};
     QuantOut ro{row_codes, row_ldc, row_sf, row_katoms, row_mask, err, nullptr};
     QuantOut co{col_codes, col_ldc, col_sf, col_katoms, nullptr, err, nullptr};
+    if (g_quant_mode == 0 && in_dtype == QT_IN_BF16 && rounding == QT_ROUND_RTN &&
+        transform == QT_TRANSFORM_RANDOMIZED && !row_mask) {
+        // tensor-core Hadamard + checked RTN (bit-identical; exact CUDA-core fallback per group)
+        int rc2 = launch_tcq_dual(x, ldx, rows, cols, row_sign_bits, col_sign_bits, prescale, ro, co,
+                                  g_quant_fallbacks, (cudaStream_t)stream);
+        return rc2 == 1001 || rc2 == 1002 ? QT_ERR_TMA : rc2;
+    }
     MxIn mx{nullptr, 0, nullptr, 0};
     return launch_quant_tile(x, in_dtype, ldx, mx, rows, cols, &rc, &ro, &cc, &co, 0, (cudaStream_t)stream);
 }

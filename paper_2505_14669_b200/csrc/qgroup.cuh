@@ -19,6 +19,7 @@
 //   * e2m1 bytes are packed with PRMT, -0 canonicalised with three LOP3/IADD per 8 nibbles.
 #pragma once
 #include "common.cuh"
+#include "launch.h"
 #include "quant.cuh"  // sr_code, quest_exact_cold (f64 reference search)
 
 namespace qt {
@@ -97,6 +98,27 @@ __device__ __forceinline__ uint32_t e2m1b(float lo, float hi) {  // byte in bits
     asm("{\n .reg .b8 t;\n cvt.rn.satfinite.e2m1x2.f32 t, %2, %1;\n cvt.u32.u8 %0, t;\n}" : "=r"(r) : "f"(lo), "f"(hi));
     return r;
 }
+// 8 values -> 4 E2M1 bytes in one register (element 2k in the low nibble of byte k): ptxas merges the
+// four conversions with F2FP.PACK_AB_MERGE_C, no byte packing instructions.
+__device__ __forceinline__ uint32_t e2m1x8(float a0, float a1, float a2, float a3, float a4, float a5, float a6,
+                                           float a7) {
+    uint32_t r;
+    asm("{\n .reg .b8 b0, b1, b2, b3;\n .reg .b16 h0, h1;\n"
+        " cvt.rn.satfinite.e2m1x2.f32 b0, %2, %1;\n cvt.rn.satfinite.e2m1x2.f32 b1, %4, %3;\n"
+        " cvt.rn.satfinite.e2m1x2.f32 b2, %6, %5;\n cvt.rn.satfinite.e2m1x2.f32 b3, %8, %7;\n"
+        " mov.b16 h0, {b0, b1};\n mov.b16 h1, {b2, b3};\n mov.b32 %0, {h0, h1};\n}"
+        : "=r"(r)
+        : "f"(a0), "f"(a1), "f"(a2), "f"(a3), "f"(a4), "f"(a5), "f"(a6), "f"(a7));
+    return r;
+}
+// E2M1 round trip of (a, b) as f16x2 grid values (exact), a in the low half
+__device__ __forceinline__ uint32_t e2m1_rt_h2(float a, float b) {
+    uint32_t h2;
+    asm("{\n .reg .b8 t;\n cvt.rn.satfinite.e2m1x2.f32 t, %2, %1;\n cvt.rn.f16x2.e2m1x2 %0, t;\n}"
+        : "=r"(h2)
+        : "f"(a), "f"(b));
+    return h2;
+}
 __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
     return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
 }
@@ -111,44 +133,58 @@ __device__ __forceinline__ uint4 encode32(const float (&v)[32], float sc) {
     uint32_t w[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        uint32_t b[4];
+        float a[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) b[k] = e2m1b(__fmul_rn(v[8 * q + 2 * k], sc), __fmul_rn(v[8 * q + 2 * k + 1], sc));
-        w[q] = canon8(pack4(b[0], b[1], b[2], b[3]));
+        for (int k = 0; k < 8; ++k) a[k] = __fmul_rn(v[8 * q + k], sc);
+        w[q] = canon8(e2m1x8(a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]));
     }
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
-// Same plus the QuEST trust mask: bit j = |v_j * sc| <= 6 (6 - |a| is negative exactly when clipped).
+// Same plus the QuEST trust mask: bit j = |v_j * sc| <= 6 (6 - |a| is negative exactly when clipped,
+// and a funnel shift collects the sign bits).
 __device__ __forceinline__ uint4 encode32_mask(const float (&v)[32], float sc, uint32_t& keep) {
     uint32_t w[4], clip = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        uint32_t b[4];
+    for (int q = 3; q >= 0; --q) {
+        float a[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float a0 = __fmul_rn(v[8 * q + 2 * k], sc), a1 = __fmul_rn(v[8 * q + 2 * k + 1], sc);
-            b[k] = e2m1b(a0, a1);
+        for (int k = 7; k >= 0; --k) {
+            a[k] = __fmul_rn(v[8 * q + k], sc);
+            clip = __funnelshift_l(__float_as_uint(__fsub_rn(6.0f, fabsf(a[k]))), clip, 1);
         }
-        w[q] = canon8(pack4(b[0], b[1], b[2], b[3]));
-    }
-#pragma unroll
-    for (int j = 31; j >= 0; --j) {
-        const float d = __fsub_rn(6.0f, fabsf(__fmul_rn(v[j], sc)));
-        clip = __funnelshift_l(__float_as_uint(d), clip, 1);
+        w[q] = canon8(e2m1x8(a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]));
     }
     keep = ~clip;
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // ------------------------------------------------------------------------------- QuEST
-// Squared FP4 rounding error of v * sc (the error is sign-symmetric, so signed values round directly).
+// q - a for a = fp32, q = the low / high f16 half of h (exact widening inside the subtraction)
+__device__ __forceinline__ float fh16_sub_lo(uint32_t h, float a) {
+    float d;
+    asm("{\n .reg .b16 l, u;\n mov.b32 {l, u}, %1;\n sub.rn.f32.f16 %0, l, %2;\n}" : "=f"(d) : "r"(h), "f"(a));
+    return d;
+}
+__device__ __forceinline__ float fh16_sub_hi(uint32_t h, float a) {
+    float d;
+    asm("{\n .reg .b16 l, u;\n mov.b32 {l, u}, %1;\n sub.rn.f32.f16 %0, u, %2;\n}" : "=f"(d) : "r"(h), "f"(a));
+    return d;
+}
+// E2M1 byte -> f16x2 grid values (exact), low nibble in the low half
+__device__ __forceinline__ uint32_t e2m1x2_to_h2(uint32_t byte) {
+    uint32_t h2;
+    asm("{\n .reg .b8 t;\n cvt.u8.u32 t, %1;\n cvt.rn.f16x2.e2m1x2 %0, t;\n}" : "=r"(h2) : "r"(byte));
+    return h2;
+}
+// Squared FP4 rounding error of v * sc (the error is sign-symmetric, so signed values round directly):
+// per element one FMUL, half an F2FP pack + unpack, one FHADD.F16 (q - a with q widened inside) and one FFMA.
 __device__ __forceinline__ float quest_err32(const float (&v)[32], float sc) {
     float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
     for (int j = 0; j < 32; j += 2) {
         const float a = __fmul_rn(v[j], sc), b = __fmul_rn(v[j + 1], sc);
-        const float2 q = e2m1x2_to_f32(e2m1b(a, b));
-        const float ta = __fsub_rn(a, q.x), tb = __fsub_rn(b, q.y);
+        const uint32_t q = e2m1_rt_h2(a, b);
+        const float ta = fh16_sub_lo(q, a), tb = fh16_sub_hi(q, b);
         acc0 = __fmaf_rn(ta, ta, acc0);
         acc1 = __fmaf_rn(tb, tb, acc1);
     }
@@ -166,21 +202,17 @@ __device__ __forceinline__ int quest_search32(const float (&v)[32], float amax, 
     const int e_hi = ceil_scale_exp(amax), e_lo = quest_low_exp(amax);
     if (e_hi <= e_lo) return e_hi;
     const float sc0 = exp2i(127 - e_hi);
-    const float E0 = quest_err32(v, sc0);
-    const float E1 = __fmul_rn(quest_err32(v, __fmul_rn(sc0, 2.0f)), 0.25f);
-    float best = E0, second = E1;
-    int bk = 0;
-    if (E1 < E0) {
-        best = E1;
-        second = E0;
-        bk = 1;
-    }
     const float a0 = __fmul_rn(amax, sc0);
-    for (int k = 2; k <= e_hi - e_lo; ++k) {
+    float best = __int_as_float(0x7f800000), second = best;
+    int bk = 0;
+    // one inlined copy of the error loop (instruction-cache footprint): k = 0, 1 always, then pruned
+    for (int k = 0; k <= e_hi - e_lo; ++k) {
         const float sk = exp2i(k), ik = exp2i(-2 * k);
-        const float d = __fsub_rn(__fmul_rn(a0, sk), 6.0f);
-        const float lb = __fmul_rn(__fmul_rn(d, d), ik);
-        if (__fmul_rn(lb, 0.99999905f) > __fadd_rn(__fmul_rn(best, 1.0f + kQTol), kQAtol)) break;
+        if (k >= 2) {
+            const float d = __fsub_rn(__fmul_rn(a0, sk), 6.0f);
+            const float lb = __fmul_rn(__fmul_rn(d, d), ik);
+            if (__fmul_rn(lb, 0.99999905f) > __fadd_rn(__fmul_rn(best, 1.0f + kQTol), kQAtol)) break;
+        }
         const float ek = __fmul_rn(quest_err32(v, __fmul_rn(sc0, sk)), ik);
         if (ek < best) {
             second = best;
@@ -215,6 +247,59 @@ __device__ __forceinline__ bool rtn_scale(float amax, float prescale, int& e, fl
     }
     sc = exp2i(127 - e);
     return false;
+}
+
+// ------------------------------------------------------------------------ group quantizer
+// Quantize one transformed group v (pre-scale NOT yet applied).  Returns the E8M0 byte.
+template <int ROUND>
+__device__ __forceinline__ int quant_group(float (&v)[32], const QuantCfg& cf, uint64_t sr_idx, int* err,
+                                           int* fallbacks, uint4& codes, uint32_t& mask) {
+    const float am = absmax32(v);
+    if (!(am <= 3.4028234663852886e38f) && err) atomicOr(err, 1);
+    mask = 0xFFFFFFFFu;
+    int e;
+    if (ROUND == kQuest) {
+        if (cf.prescale != 1.0f) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], cf.prescale);
+        }
+        const float amp = cf.prescale != 1.0f ? __fmul_rn(am, cf.prescale) : am;
+        if (amp > 0.0f && amp <= 3.4028234663852886e38f) {
+            e = quest_search32(v, amp, fallbacks);
+            codes = encode32_mask(v, exp2i(127 - e), mask);
+        } else {
+            e = 0;  // zero group: e = 0, codes 0, all kept (_native.pyx:228-233)
+            codes = make_uint4(0, 0, 0, 0);
+        }
+    } else if (ROUND == kRtn) {
+        float sc;
+        if (!rtn_scale(am, cf.prescale, e, sc)) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], cf.prescale);
+        }
+        codes = encode32(v, sc);
+    } else {
+        if (cf.prescale != 1.0f) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], cf.prescale);
+        }
+        e = ceil_scale_exp(cf.prescale != 1.0f ? __fmul_rn(am, cf.prescale) : am);
+        const float sc_f = exp2i(127 - e);
+        const double sc_d = (double)sc_f;
+        uint32_t w[4];
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int j = qq * 8 + k;
+                acc |= sr_code(v[j], sc_f, sc_d, cf.sr_base, sr_idx + (uint64_t)j) << (4 * k);
+            }
+            w[qq] = acc;
+        }
+        codes = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    return e;
 }
 
 }  // namespace qt

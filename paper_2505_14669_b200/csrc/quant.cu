@@ -208,13 +208,17 @@ __device__ __forceinline__ void load_col_pair(const uint4* tile, int cp, int q, 
     using G = Geom<IN>;
     const int r0 = q * 32;
     if (IN == kInBF16) {
-        const uint32_t* t32 = reinterpret_cast<const uint32_t*>(tile);
-        const int kc = cp >> 2, wd = cp & 3;
+        const uint32_t* t32 = reinterpret_cast<const uint32_t*>(tile) + r0 * G::CPR * 4 + (cp & 3);
+        const int kc = cp >> 2;
+        // the swizzle of row q*32 + i depends on (i + q) & 3 only: 4 word offsets, hoisted
+        int off[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) off[m] = tile_chunk<2>(r0 + m, kc) * 4;
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
             const int r = r0 + i;
-            uint32_t w0 = t32[(r * G::CPR + tile_chunk<2>(r, kc)) * 4 + wd];
-            uint32_t w1 = t32[((r + 1) * G::CPR + tile_chunk<2>(r + 1, kc)) * 4 + wd];
+            uint32_t w0 = t32[i * G::CPR * 4 + off[i & 3]];
+            uint32_t w1 = t32[(i + 1) * G::CPR * 4 + off[(i + 1) & 3]];
             if (transform == kRandomized) {
                 const uint2 m = *reinterpret_cast<const uint2*>(clut + r);
                 w0 ^= m.x;
@@ -282,62 +286,9 @@ __device__ __forceinline__ void load_col_codes(const uint8_t* codes, const float
     }
 }
 
-// ------------------------------------------------------------------------ group quantizer
-// Quantize one transformed group v (pre-scale NOT yet applied).  Returns the E8M0 byte.
-template <int ROUND>
-__device__ __forceinline__ int quant_group(float (&v)[32], const QuantCfg& cf, uint64_t sr_idx, int* err,
-                                           int* fallbacks, uint4& codes, uint32_t& mask) {
-    const float am = absmax32(v);
-    if (!(am <= 3.4028234663852886e38f) && err) atomicOr(err, 1);
-    mask = 0xFFFFFFFFu;
-    int e;
-    if (ROUND == kQuest) {
-        if (cf.prescale != 1.0f) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], cf.prescale);
-        }
-        const float amp = cf.prescale != 1.0f ? __fmul_rn(am, cf.prescale) : am;
-        if (amp > 0.0f && amp <= 3.4028234663852886e38f) {
-            e = quest_search32(v, amp, fallbacks);
-            codes = encode32_mask(v, exp2i(127 - e), mask);
-        } else {
-            e = 0;  // zero group: e = 0, codes 0, all kept (_native.pyx:228-233)
-            codes = make_uint4(0, 0, 0, 0);
-        }
-    } else if (ROUND == kRtn) {
-        float sc;
-        if (!rtn_scale(am, cf.prescale, e, sc)) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], cf.prescale);
-        }
-        codes = encode32(v, sc);
-    } else {
-        if (cf.prescale != 1.0f) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], cf.prescale);
-        }
-        e = ceil_scale_exp(cf.prescale != 1.0f ? __fmul_rn(am, cf.prescale) : am);
-        const float sc_f = exp2i(127 - e);
-        const double sc_d = (double)sc_f;
-        uint32_t w[4];
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-            uint32_t acc = 0;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int j = qq * 8 + k;
-                acc |= sr_code(v[j], sc_f, sc_d, cf.sr_base, sr_idx + (uint64_t)j) << (4 * k);
-            }
-            w[qq] = acc;
-        }
-        codes = make_uint4(w[0], w[1], w[2], w[3]);
-    }
-    return e;
-}
-
 // ------------------------------------------------------------------------------- kernel
 template <int IN, int ROW, int COL, int CROUND>
-__global__ void __launch_bounds__(256, IN == kInF32 ? 1 : 2) k_quant(TileArgs a) {
+__global__ void __launch_bounds__(256, 2) k_quant(TileArgs a) {
     using G = Geom<IN>;
     constexpr int TR = G::TR;
     extern __shared__ __align__(16) uint8_t smem[];

@@ -260,3 +260,59 @@ def test_fused_forward_equals_rows_then_requant(qt, shape, dtype, col_round, row
     assert torch.equal(row.mask, ref_row.mask)
     assert torch.equal(col.codes, ref_col.codes)
     assert torch.equal(col.scales_rowmajor(), ref_col.scales_rowmajor())
+
+
+def _dual_inputs():
+    g = torch.Generator(device="cuda").manual_seed(3)
+    yield "gauss", torch.randn(512, 384, device="cuda", generator=g)
+    yield "ragged", torch.randn(96, 160, device="cuda", generator=g) * 1e-3
+    t = torch.distributions.StudentT(1.0).sample((256, 256)).cuda()
+    yield "t1", t
+    x = torch.randn(256, 128, device="cuda", generator=g)
+    x[:, ::7] *= 1e6
+    x[3] = 0
+    x[5, :64] = 0.25
+    yield "outliers", x
+    yield "grid", (torch.randint(-12, 13, (128, 256), device="cuda", generator=g).float() * 0.25)
+    yield "wide", torch.randn(128, 128, device="cuda", generator=g) * torch.exp2(
+        torch.randint(-60, 60, (128, 128), device="cuda", generator=g).float())
+    yield "large", torch.randn(4096, 1024, device="cuda", generator=g)
+
+
+@pytest.mark.parametrize("case", ["gauss", "ragged", "t1", "outliers", "grid", "wide", "large"])
+def test_tensor_core_dual_equals_exact_path(qt, oracle, case):
+    """The tcgen05 Hadamard quantizer (checked RTN + exact per-group fallback) is bit-identical to the
+    CUDA-core path (itself pinned to the oracle) -- and, for the small cases, to the oracle directly."""
+    from paper_2505_14669_b200 import _lib
+    from paper_2505_14669_b200.mxfp4 import quant_dual, sign_bits
+
+    x = dict(_dual_inputs())[case].to(torch.bfloat16)
+    R, C = x.shape
+    rs, cs = sign_bits(5, C, "cuda"), sign_bits(9, R, "cuda", start=32)
+    L = _lib.load()
+    fb = torch.zeros(1, dtype=torch.int32, device="cuda")
+    outs = []
+    for mode in (0, 1):
+        L.qt_debug_set_quant(mode, fb.data_ptr())
+        try:
+            outs.append(quant_dual(x, _lib.QT_ROUND_RTN, transform=_lib.QT_TRANSFORM_RANDOMIZED, signs=rs,
+                                   col_signs=cs, prescale=0.75))
+        finally:
+            L.qt_debug_set_quant(0, None)
+    torch.cuda.synchronize()
+    (g0, gt0), (g1, gt1) = outs
+    for a, b in ((g0, g1), (gt0, gt1)):
+        assert torch.equal(a.codes, b.codes)
+        assert torch.equal(a.scales_rowmajor(), b.scales_rowmajor())
+    groups = 2 * R * C // 32
+    print(f"{case}: {int(fb.item())} of {groups} groups re-decided exactly")
+    if R * C <= 512 * 384:
+        xf = x.float().cpu().numpy()
+        s_c = np.array(oracle.signs(5, 0, C), np.float32)
+        s_r = np.array(oracle.signs(9, 32, R), np.float32)
+        gh = oracle.fwht(xf * s_c[None, :], 32) * np.float32(0.75)
+        c, s = oracle.quantize_rtn(gh.astype(np.float64), 32)
+        assert_operand_equal(g0, c, s, "G")
+        gth = oracle.fwht(np.ascontiguousarray(xf.T) * s_r[None, :], 32) * np.float32(0.75)
+        c, s = oracle.quantize_rtn(gth.astype(np.float64), 32)
+        assert_operand_equal(gt0, c, s, "G_t")
