@@ -15,7 +15,10 @@ static int* g_quant_fallbacks = nullptr;
 
 extern "C" {
 
-void qt_debug_set_gemm(int dbg) { g_gemm_dbg = dbg; }
+void qt_debug_set_gemm(int dbg) {
+    g_gemm_dbg = dbg & 0xFFFF;
+    qt::g_gemm_2sm = (dbg & 0x20000) ? 1 : 0;  // bit 17: use the 2-CTA kernel
+}
 
 void qt_debug_set_quant(int mode, int* fallbacks) {
     qt::g_tcq_dbg = mode >> 4;

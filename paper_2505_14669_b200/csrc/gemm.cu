@@ -36,6 +36,63 @@ struct GemmSmem {
     static constexpr int TMEM_COLS = BN == 256 ? 512 : 256;
 };
 
+// Epilogue of one accumulator row slice: columns cbase .. cbase + CW - 1 of output row `row`, held as
+// CW/32 chunks of 32 fp32 values (tcgen05.ld 32x32b); per 64-column pair of chunks (packed f32x2):
+// mask multiply, bit-exact FWHT-32 along N, scale, bf16 / fp32 store.
+template <int CW>
+__device__ __forceinline__ void epi_store(const uint32_t (&acc)[CW / 32][32], int row, int cbase, int N,
+                                          const EpiParams& ep, float2 nz) {
+#pragma unroll
+    for (int pj = 0; pj < CW / 64; ++pj) {
+        const int col0 = cbase + pj * 64;  // columns col0 .. col0+63: chunk A, chunk B
+        if (col0 >= N) break;
+        const bool okB = col0 + 32 < N;
+        Pair g;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            g.p[i] = make_float2(__uint_as_float(acc[2 * pj][i]), __uint_as_float(acc[2 * pj + 1][i]));
+        if (ep.mode != kEpiStore) {
+            const uint32_t mA = __ldg(ep.mask + (int64_t)row * ep.ldm + col0 / 32);
+            const uint32_t mB = okB ? __ldg(ep.mask + (int64_t)row * ep.ldm + col0 / 32 + 1) : 0u;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                g.p[i].x = ((mA >> i) & 1u) ? g.p[i].x : 0.0f;
+                g.p[i].y = ((mB >> i) & 1u) ? g.p[i].y : 0.0f;
+            }
+            if (ep.mode == kEpiMaskH) fwht_pair(g, nz);
+            scale_pair(g, ep.scale);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !okB) break;
+            const int col = col0 + 32 * h;
+            if (ep.out_bf16) {
+                uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) + (int64_t)row * ep.ldo + col);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int i = q * 8 + 2 * t;
+                        __nv_bfloat162 b2 = h ? __floats2bfloat162_rn(g.p[i].y, g.p[i + 1].y)
+                                              : __floats2bfloat162_rn(g.p[i].x, g.p[i + 1].x);
+                        w[t] = *reinterpret_cast<uint32_t*>(&b2);
+                    }
+                    o[q] = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            } else {
+                float4* o = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + (int64_t)row * ep.ldo + col);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int i = 4 * q;
+                    o[q] = h ? make_float4(g.p[i].y, g.p[i + 1].y, g.p[i + 2].y, g.p[i + 3].y)
+                             : make_float4(g.p[i].x, g.p[i + 1].x, g.p[i + 2].x, g.p[i + 3].x);
+                }
+            }
+        }
+    }
+}
+
 // Persistent tcgen05 GEMM: one CTA per SM walks tiles blockIdx.x, blockIdx.x + gridDim.x, ...
 // The TMA producer runs ahead across tile boundaries (its ring never drains), the MMA warp starts
 // tile i+1 as soon as the epilogue warps have copied tile i's accumulator out of TMEM into
@@ -108,28 +165,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {
+            // scale factors double-buffered in TMEM (set it & 1); with dbg bit 5 the copies of k-tile it + 1
+            // are issued BEFORE the MMAs of k-tile it (those MMAs read the other set), so a copy's latency
+            // need not sit between two dependent MMAs
+            const bool pre = (ep.dbg & 32) != 0;
+            auto sf_copy = [&](int itx) {
+                const int sx = itx % kStages;
+                const uint32_t a_sf = smem_u32(sSFA + sx * L::SFA), b_sf = smem_u32(sSFB + sx * L::SFB);
+                const uint32_t ta = t_sfa + (pre ? (itx & 1) * 32 : 0), tb = t_sfb + (pre ? (itx & 1) * 32 : 0);
+                tmem_cp_sf(ta + 0, make_sdesc(a_sf, 0, 128, kLayoutNone));
+                tmem_cp_sf(ta + 4, make_sdesc(a_sf + 512, 0, 128, kLayoutNone));
+#pragma unroll
+                for (int rb = 0; rb < BN / 128; ++rb) {
+                    tmem_cp_sf(tb + rb * 4, make_sdesc(b_sf + rb * 1024, 0, 128, kLayoutNone));
+                    tmem_cp_sf(tb + (BN / 128) * 4 + rb * 4, make_sdesc(b_sf + rb * 1024 + 512, 0, 128, kLayoutNone));
+                }
+            };
+            const int my_tiles = tiles > (int)blockIdx.x ? (tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+            const int total = my_tiles * nk;
             int it = 0, tcount = 0;
+            if (pre && total > 0) {
+                mbar_wait(&full[0], 0);
+                tc_fence_after();
+                sf_copy(0);
+            }
             for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
                 mbar_wait(tmem_empty, (tcount & 1) ^ 1);  // epilogue has drained the accumulator
                 tc_fence_after();
                 for (int kt = 0; kt < nk; ++kt, ++it) {
                     const int s = it % kStages;
-                    const uint32_t ph = (it / kStages) & 1;
-                    mbar_wait(&full[s], ph);
+                    mbar_wait(&full[s], (it / kStages) & 1);
                     tc_fence_after();
-                    // scale factors -> TMEM (executes in order with the MMAs below)
-                    const uint32_t a_sf = smem_u32(sSFA + s * L::SFA), b_sf = smem_u32(sSFB + s * L::SFB);
-                    if (!((ep.dbg & 1) && kt > 0)) {
-                    tmem_cp_sf(t_sfa + 0, make_sdesc(a_sf, 0, 128, kLayoutNone));
-                    tmem_cp_sf(t_sfa + 4, make_sdesc(a_sf + 512, 0, 128, kLayoutNone));
-#pragma unroll
-                    for (int rb = 0; rb < BN / 128; ++rb) {
-                        tmem_cp_sf(t_sfb + rb * 4, make_sdesc(b_sf + rb * 1024, 0, 128, kLayoutNone));
-                        tmem_cp_sf(t_sfb + (BN / 128) * 4 + rb * 4,
-                                   make_sdesc(b_sf + rb * 1024 + 512, 0, 128, kLayoutNone));
-                    }
+                    if (!pre) {
+                        if (!((ep.dbg & 1) && kt > 0)) sf_copy(it);
+                    } else if (it + 1 < total) {
+                        const int s1 = (it + 1) % kStages;
+                        mbar_wait(&full[s1], ((it + 1) / kStages) & 1);
+                        tc_fence_after();
+                        sf_copy(it + 1);
                     }
                     const uint32_t a_base = smem_u32(sA + s * L::A), b_base = smem_u32(sB + s * L::B);
+                    const uint32_t ta = t_sfa + (pre ? (it & 1) * 32 : 0), tb = t_sfb + (pre ? (it & 1) * 32 : 0);
                     const int nmma = (ep.dbg & 4) ? 1 : 4;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
@@ -137,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint64_t ad = make_sdesc(a_base + j * 32, 0, 1024, kLayoutSW128);
                         const uint64_t bd = make_sdesc(b_base + j * 32, 0, 1024, kLayoutSW128);
                         const uint32_t id = idesc_mxf4(kBM, BN, (j & 1) * 2, (j & 1) * 2);
-                        mma_mxf4(t_acc, ad, bd, id, t_sfa + (j >> 1) * 4, t_sfb + (j >> 1) * (BN / 128) * 4,
+                        mma_mxf4(t_acc, ad, bd, id, ta + (j >> 1) * 4, tb + (j >> 1) * (BN / 128) * 4,
                                  (kt | j) != 0 ? 1u : 0u);
                     }
                     tc_commit(&empty[s]);
@@ -164,56 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(tmem_empty);  // the MMA warp may start the next tile now
             if (row >= M) continue;
-#pragma unroll
-            for (int pj = 0; pj < CW / 64; ++pj) {
-                const int col0 = cbase + pj * 64;  // columns col0 .. col0+63: chunk A, chunk B
-                if (col0 >= N) break;
-                const bool okB = col0 + 32 < N;
-                Pair g;
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    g.p[i] = make_float2(__uint_as_float(acc[2 * pj][i]), __uint_as_float(acc[2 * pj + 1][i]));
-                if (ep.mode != kEpiStore) {
-                    const uint32_t mA = __ldg(ep.mask + (int64_t)row * ep.ldm + col0 / 32);
-                    const uint32_t mB = okB ? __ldg(ep.mask + (int64_t)row * ep.ldm + col0 / 32 + 1) : 0u;
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        g.p[i].x = ((mA >> i) & 1u) ? g.p[i].x : 0.0f;
-                        g.p[i].y = ((mB >> i) & 1u) ? g.p[i].y : 0.0f;
-                    }
-                    if (ep.mode == kEpiMaskH) fwht_pair(g, nz);
-                    scale_pair(g, ep.scale);
-                }
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (h == 1 && !okB) break;
-                    const int col = col0 + 32 * h;
-                    if (ep.out_bf16) {
-                        uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) +
-                                                            (int64_t)row * ep.ldo + col);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            uint32_t w[4];
-#pragma unroll
-                            for (int t = 0; t < 4; ++t) {
-                                const int i = q * 8 + 2 * t;
-                                __nv_bfloat162 b2 = h ? __floats2bfloat162_rn(g.p[i].y, g.p[i + 1].y)
-                                                      : __floats2bfloat162_rn(g.p[i].x, g.p[i + 1].x);
-                                w[t] = *reinterpret_cast<uint32_t*>(&b2);
-                            }
-                            o[q] = make_uint4(w[0], w[1], w[2], w[3]);
-                        }
-                    } else {
-                        float4* o = reinterpret_cast<float4*>(static_cast<float*>(ep.out) + (int64_t)row * ep.ldo + col);
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const int i = 4 * q;
-                            o[q] = h ? make_float4(g.p[i].y, g.p[i + 1].y, g.p[i + 2].y, g.p[i + 3].y)
-                                     : make_float4(g.p[i].x, g.p[i + 1].x, g.p[i + 2].x, g.p[i + 3].x);
-                        }
-                    }
-                }
-            }
+            epi_store<CW>(acc, row, cbase, N, ep, nz);
         }
     }
     __syncthreads();
@@ -223,7 +250,199 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+
+// ------------------------------------------------------------------ 2-CTA (cta_group::2) GEMM
+// A CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile with tcgen05.mma.cta_group::2
+// (M = 256, N = 256, K = 64): CTA r holds A rows m0 + 128 r and B rows n0 + 128 r of each K tile (so
+// every SM stages half the B bytes of the 1-CTA kernel per FLOP) plus the scale factors of its A rows
+// and of all 256 B rows (the scale-factor TMEM layout is the 1-SM one, duplicated per CTA).  Only the
+// leader (rank 0) issues MMAs and scale-factor copies (cta_group::2 acts on both CTAs); both CTAs'
+// TMA loads complete on the leader's full barrier, MMA commits multicast to both CTAs' barriers.
+namespace sm2 {
+constexpr int kStages = 6;
+constexpr int kA = 128 * kBKBytes;     // own 128 A rows
+constexpr int kB = 128 * kBKBytes;     // own 128 of the 256 B rows
+constexpr int kSFA = 1024;             // own 128 rows x 8 groups
+constexpr int kSFB = 2048;             // all 256 B rows x 8 groups
+constexpr int kStage = kA + kB + kSFA + kSFB;
+constexpr int kBytes = kStages * kStage + 1024 + 256;
+}  // namespace sm2
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// 2-SM TMA: data lands in this CTA's smem, completion bytes on the (leader's) barrier `mbar_cluster`
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t mbar_cluster, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(mbar_cluster), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void mma_mxf4_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t sfa_tmem, uint32_t sfb_tmem, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa_tmem), "r"(sfb_tmem));
+}
+__device__ __forceinline__ void tmem_cp_sf_2sm(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc));
+}
+__device__ __forceinline__ void tc_commit_2sm(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    k_gemm_mxf4_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB, int M, int N,
+                    int K, EpiParams ep) {
+    constexpr int BN = 256, CW = BN / 2;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = sA + sm2::kStages * sm2::kA;
+    uint8_t* sSFA = sB + sm2::kStages * sm2::kB;
+    uint8_t* sSFB = sSFA + sm2::kStages * sm2::kSFA;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sSFB + sm2::kStages * sm2::kSFB);
+    uint64_t* empty = full + sm2::kStages;
+    uint64_t* tmem_full = empty + sm2::kStages;
+    uint64_t* tmem_empty = tmem_full + 1;
+    uint32_t* tmem_base_holder = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int nk = (K + 255) / 256;
+    const int tiles_n = (N + BN - 1) / BN, tiles = ((M + 255) / 256) * tiles_n;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmA);
+        tma_prefetch(&tmB);
+        tma_prefetch(&tmSFA);
+        tma_prefetch(&tmSFB);
+        for (int s = 0; s < sm2::kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        mbar_init(tmem_empty, 2 * kEpiWarps);
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_holder)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_base_holder;
+    const uint32_t t_acc = tmem, t_sfa = tmem + BN, t_sfb = tmem + BN + 8;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0;
+            for (int tile = cid; tile < tiles; tile += ncl) {
+                const int m0 = (tile / tiles_n) * 256 + 128 * rank, n0 = (tile % tiles_n) * BN;
+                for (int kt = 0; kt < nk; ++kt, ++it) {
+                    const int s = it % sm2::kStages;
+                    mbar_wait(&empty[s], ((it / sm2::kStages) & 1) ^ 1);
+                    const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+                    if (leader) mbar_arrive_expect_tx(&full[s], 2 * sm2::kStage);
+                    tma_load_2d_2sm(sA + s * sm2::kA, &tmA, fb, kt * kBKBytes, m0);
+                    tma_load_2d_2sm(sB + s * sm2::kB, &tmB, fb, kt * kBKBytes, n0 + 128 * (int)rank);
+                    // scale atoms (u32 view, 1 KB = 256 words per K tile): A rows of this CTA, all 256 B rows
+                    tma_load_2d_2sm(sSFA + s * sm2::kSFA, &tmSFA, fb, kt * 256, m0 / 128);
+                    tma_load_2d_2sm(sSFB + s * sm2::kSFB, &tmSFB, fb, kt * 256, n0 / 128);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            int it = 0, tcount = 0;
+            for (int tile = cid; tile < tiles; tile += ncl, ++tcount) {
+                mbar_wait(tmem_empty, (tcount & 1) ^ 1);  // both CTAs' epilogues drained the accumulator
+                tc_fence_after();
+                for (int kt = 0; kt < nk; ++kt, ++it) {
+                    const int s = it % sm2::kStages;
+                    mbar_wait(&full[s], (it / sm2::kStages) & 1);
+                    tc_fence_after();
+                    const uint32_t a_sf = smem_u32(sSFA + s * sm2::kSFA), b_sf = smem_u32(sSFB + s * sm2::kSFB);
+                    if (!((ep.dbg & 1) && kt > 0)) {
+                    tmem_cp_sf_2sm(t_sfa + 0, make_sdesc(a_sf, 0, 128, kLayoutNone));
+                    tmem_cp_sf_2sm(t_sfa + 4, make_sdesc(a_sf + 512, 0, 128, kLayoutNone));
+#pragma unroll
+                    for (int rb = 0; rb < 2; ++rb) {
+                        tmem_cp_sf_2sm(t_sfb + rb * 4, make_sdesc(b_sf + rb * 1024, 0, 128, kLayoutNone));
+                        tmem_cp_sf_2sm(t_sfb + 8 + rb * 4, make_sdesc(b_sf + rb * 1024 + 512, 0, 128, kLayoutNone));
+                    }
+                    }
+                    const uint32_t a_base = smem_u32(sA + s * sm2::kA), b_base = smem_u32(sB + s * sm2::kB);
+                    const int nmma = (ep.dbg & 4) ? 1 : 4;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (j >= nmma) break;
+                        const uint64_t ad = make_sdesc(a_base + j * 32, 0, 1024, kLayoutSW128);
+                        const uint64_t bd = make_sdesc(b_base + j * 32, 0, 1024, kLayoutSW128);
+                        mma_mxf4_2sm(t_acc, ad, bd, idesc_mxf4(256, BN, (j & 1) * 2, (j & 1) * 2),
+                                     t_sfa + (j >> 1) * 4, t_sfb + (j >> 1) * 8, (kt | j) != 0 ? 1u : 0u);
+                    }
+                    tc_commit_2sm(&empty[s]);
+                }
+                tc_commit_2sm(tmem_full);
+            }
+        }
+    } else {
+        const int quad = warp % 4, half = (warp - 2) / 4;
+        const float2 nz = opaque_nz2();
+        const uint32_t te_leader = mapa_shared(smem_u32(tmem_empty), 0);
+        int tcount = 0;
+        for (int tile = cid; tile < tiles; tile += ncl, ++tcount) {
+            const int m0 = (tile / tiles_n) * 256 + 128 * rank, n0 = (tile % tiles_n) * BN;
+            const int row = m0 + quad * 32 + lane, cbase = n0 + half * CW;
+            mbar_wait(tmem_full, tcount & 1);
+            tc_fence_after();
+            uint32_t acc[CW / 32][32];
+#pragma unroll
+            for (int c = 0; c < CW / 32; ++c)
+                tmem_ld32(t_acc + ((uint32_t)(quad * 32) << 16) + half * CW + c * 32, acc[c]);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(te_leader);  // the leader may start the next tile
+            if (row >= M) continue;
+            epi_store<CW>(acc, row, cbase, N, ep, nz);
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
 // ---------------------------------------------------------------------------- host side
+int g_gemm_2sm = 0;  // 1: use the 2-CTA kernel where eligible (measured no faster yet: see DESIGN.md)
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -280,10 +499,49 @@ static int launch_gemm_bn(const uint8_t* a, int64_t lda, const uint8_t* a_sf, in
     return (int)cudaGetLastError();
 }
 
+// scale atoms viewed as u32 [row blocks][katoms * 128]; box 256 words (one K tile) x box_rows blocks
+static int make_sf_map(CUtensorMap* m, const uint8_t* sf, int64_t rows, int64_t katoms, int box_rows) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return 1001;
+    const int64_t rb = ((rows + 255) / 256) * 2;
+    cuuint64_t dims[2] = {(cuuint64_t)(katoms * 128), (cuuint64_t)rb};
+    cuuint64_t strides[1] = {(cuuint64_t)(katoms * 512)};
+    cuuint32_t box[2] = {256, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, (void*)sf, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : 1002;
+}
+
+static int launch_gemm_2sm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, int64_t a_katoms, const uint8_t* b,
+                           int64_t ldb, const uint8_t* b_sf, int64_t b_katoms, int64_t M, int64_t N, int64_t K,
+                           const EpiParams& ep, cudaStream_t st) {
+    CUtensorMap ta, tb, tsa, tsb;
+    int rc = make_codes_map(&ta, a, M, K / 2, lda, 128);
+    if (!rc) rc = make_codes_map(&tb, b, N, K / 2, ldb, 128);
+    if (!rc) rc = make_sf_map(&tsa, a_sf, M, a_katoms, 1);
+    if (!rc) rc = make_sf_map(&tsb, b_sf, N, b_katoms, 2);
+    if (rc) return rc;
+    static int sms = 0;
+    if (!sms) {
+        cudaFuncSetAttribute(k_gemm_mxf4_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2::kBytes);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t tiles = ((M + 255) / 256) * ((N + 255) / 256);
+    const int64_t pairs = tiles < sms / 2 ? tiles : sms / 2;
+    k_gemm_mxf4_2sm<<<(unsigned)(2 * pairs), kThreads, sm2::kBytes, st>>>(ta, tb, tsa, tsb, (int)M, (int)N, (int)K, ep);
+    return (int)cudaGetLastError();
+}
+
 int launch_gemm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, int64_t a_katoms, const uint8_t* b, int64_t ldb,
                 const uint8_t* b_sf, int64_t b_katoms, int64_t M, int64_t N, int64_t K, const EpiParams& ep,
                 cudaStream_t st) {
     if (M == 0 || N == 0) return 0;
+    if (g_gemm_2sm && N % 256 == 0 && M >= 256)
+        return launch_gemm_2sm(a, lda, a_sf, a_katoms, b, ldb, b_sf, b_katoms, M, N, K, ep, st);
     if (N >= 256 && N % 256 == 0)
         return launch_gemm_bn<256>(a, lda, a_sf, a_katoms, b, ldb, b_sf, b_katoms, M, N, K, ep, st);
     return launch_gemm_bn<128>(a, lda, a_sf, a_katoms, b, ldb, b_sf, b_katoms, M, N, K, ep, st);

@@ -101,3 +101,16 @@ def test_gemm_mask_hadamard_epilogue(qt, oracle):
     assert np.array_equal(got, ref)   # same fp32 accumulator -> epilogue must be bit-exact
     got_nh = qt.gemm(A, B, mask=mask, hadamard=False, scale=float(post)).cpu().numpy()
     assert np.array_equal(got_nh, (plain * m).astype(np.float32) * post)
+
+
+@pytest.mark.parametrize("mnk", [(256, 256, 256), (512, 768, 1024), (2048, 1024, 2304)])
+def test_gemm_2cta_kernel(qt, oracle, mnk):
+    """The cta_group::2 kernel (256 x 256 pair tiles) matches the oracle like the 1-CTA kernel."""
+    from paper_2505_14669_b200 import _lib
+
+    L = _lib.load()
+    L.qt_debug_set_gemm(0x20000)
+    try:
+        test_gemm_random(qt, oracle, mnk)
+    finally:
+        L.qt_debug_set_gemm(0)
