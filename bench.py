@@ -363,6 +363,26 @@ def run_ours(args, rank, world, local_rank):
     }
 
 
+def run_train(rank, world, local_rank):
+    """BASELINE configs 2 / 4 / 5 through the Llama-Quartet stack (all linears MXFP4): Llama-200M data-parallel
+    training throughput (64 x 512 tokens per GPU, bf16 NCCL gradient all-reduce), one Llama-30M training step,
+    and one Llama-7B-dims transformer block fwd+bwd at 8k sequence x batch 4 (per GPU)."""
+    import torch
+
+    from paper_2505_14669_b200 import llama
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
+    from train_llama import run
+
+    dev = torch.device("cuda", local_rank)
+    out = {"data": "synthetic token streams (no datasets offline)",
+           "optimizer": "AdamW 0.9/0.95 wd 0.1, clip 1.0, warmup+cosine (train.py:58-85, 325-382)"}
+    out["llama200m_dp"] = run(llama, "200m", 64, 5, 2, False, dev, world, rank)
+    out["llama30m"] = run(llama, "30m", 64, 3, 1, False, dev, world, rank)
+    out["block7b_8k_b4"] = run(llama, "7b", 4, 3, 1, True, dev, world, rank)
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_reference(args, rank, world):
     """Reference CPU implementation of the path (oracle port of mx4train's native kernels), all host
     threads.  Each step is a bounded sample of the workload: one fwd+bwd of one of the three shapes
@@ -426,6 +446,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from Python each step")
+    ap.add_argument("--no-train", action="store_true", help="skip the Llama training-throughput section")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -445,6 +466,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     out = run_ours(args, rank, world, local_rank)
+    if not args.no_train:
+        tr = run_train(rank, world, local_rank)
+        if out is not None:
+            out["train"] = tr
     if out is not None and world == 1 and not args.no_cpu_baseline:
         r = cpu_baseline_sample(1, 128)
         out["cpu_baseline"] = {"value": round(r["flop"] / r["seconds"] / 1e12, 6), "unit": "TFLOP/s", "cores": 1,

@@ -1,0 +1,224 @@
+"""Llama-style causal LM whose every linear layer is a Quartet MXFP4 layer (BASELINE configs 2, 4, 5).
+
+The caller of the hot path: token embedding -> N x [RMSNorm -> attention (q, k, v,
+o: QuartetLinear, RoPE, causal SDPA in bf16) -> RMSNorm -> SwiGLU MLP (gate, up, down: QuartetLinear)]
+-> RMSNorm -> LM head (QuartetLinear).  Attention and norms stay in bf16/fp32 torch; every matmul with a
+weight runs through libquartet_b200 (forward QuEST + H32, backward RHT + RTN/SR, tcgen05 MXFP4 GEMMs).
+
+Training follows the reference's loop semantics (mx4train/train.py:58-85, 325-382) at Llama scale:
+AdamW (beta 0.9 / 0.95, eps 1e-8, decoupled weight decay 0.1) on fp32 master weights, global-norm
+clipping at 1.0, linear warm-up over 10 % of the steps then cosine decay (lr_at, train.py:76-85), and a
+fresh backward seed per step and layer (derive_seed(derive_seed(seed, 4, step), layer), train.py:346-348).
+Model shapes follow PAPER.md Appendix (hyper-parameter table): 30M = 6 x 640 (5 heads), 200M = 10 x 1280
+(10 heads), sequence 512; the 7B block uses the Llama-2-7B dims 4096 / 11008 / 32 heads.
+
+Data parallelism: one process per GPU; each rank holds whole sequences, so the only exchange is the
+gradient all-reduce (bf16 on the wire, NCCL over NVLink), done once per step over one flat bucket.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+import torch.nn.functional as F
+
+from .nn import QuartetLinear
+
+GROUP = 32
+
+
+@dataclass(frozen=True)
+class LlamaConfig:
+    n_layer: int
+    d_model: int
+    n_head: int
+    vocab: int = 32000
+    seq_len: int = 512
+    d_ff: int | None = None          # SwiGLU hidden size; default 8/3 d rounded up to 256
+    rounding: str = "rtn"
+    rope_base: float = 10000.0
+
+    @property
+    def hidden(self) -> int:
+        if self.d_ff is not None:
+            return self.d_ff
+        h = int(8 * self.d_model / 3)
+        return (h + 255) // 256 * 256
+
+    def n_params(self, embeddings: bool = False) -> int:
+        d, h = self.d_model, self.hidden
+        n = self.n_layer * (4 * d * d + 3 * d * h + 2 * d) + d
+        return n + (2 * self.vocab * d if embeddings else 0)
+
+
+PRESETS = {
+    "30m": LlamaConfig(n_layer=6, d_model=640, n_head=5),
+    "50m": LlamaConfig(n_layer=7, d_model=768, n_head=6),
+    "100m": LlamaConfig(n_layer=8, d_model=1024, n_head=8),
+    "200m": LlamaConfig(n_layer=10, d_model=1280, n_head=10),
+    "7b": LlamaConfig(n_layer=32, d_model=4096, n_head=32, d_ff=11008, seq_len=8192),
+}
+PAPER_LR = {"30m": 1.2e-3, "50m": 1.2e-3, "100m": 6e-4, "200m": 3e-4, "7b": 9.375e-6}
+
+
+class RMSNorm(torch.nn.Module):
+    def __init__(self, d: int, eps: float = 1e-6, device=None):
+        super().__init__()
+        self.weight = torch.nn.Parameter(torch.ones(d, device=device))
+        self.eps = eps
+
+    def forward(self, x):  # fused torch kernel in bf16 (fp32 statistics)
+        return F.rms_norm(x.to(torch.bfloat16), (x.shape[-1],), self.weight.to(torch.bfloat16), self.eps)
+
+
+def _rope(seq: int, dh: int, base: float, device):
+    """Rotary tables in the half-split (GPT-NeoX) layout, bf16 [seq, dh]."""
+    inv = 1.0 / (base ** (torch.arange(0, dh, 2, device=device, dtype=torch.float32) / dh))
+    t = torch.arange(seq, device=device, dtype=torch.float32)
+    f = torch.outer(t, inv)
+    f = torch.cat((f, f), dim=-1)
+    return torch.cos(f).to(torch.bfloat16), torch.sin(f).to(torch.bfloat16)
+
+
+def _apply_rope(x, cos, sin):  # x [B, H, S, dh] bf16
+    h = x.shape[-1] // 2
+    rot = torch.cat((-x[..., h:], x[..., :h]), dim=-1)
+    S = x.shape[2]
+    return x * cos[:S] + rot * sin[:S]
+
+
+class Block(torch.nn.Module):
+    def __init__(self, cfg: LlamaConfig, index: int, seed: int, device=None):
+        super().__init__()
+        d, h = cfg.d_model, cfg.hidden
+        lid = 16 * index
+
+        def ql(i, o, k):
+            return QuartetLinear(i, o, seed=seed, layer_id=lid + k, rounding=cfg.rounding, device=device)
+
+        self.n_head = cfg.n_head
+        self.attn_norm, self.mlp_norm = RMSNorm(d, device=device), RMSNorm(d, device=device)
+        self.q, self.k, self.v, self.o = ql(d, d, 0), ql(d, d, 1), ql(d, d, 2), ql(d, d, 3)
+        self.gate, self.up, self.down = ql(d, h, 4), ql(d, h, 5), ql(h, d, 6)
+
+    def forward(self, x, cos, sin):  # x [B, S, d] bf16
+        B, S, d = x.shape
+        H, dh = self.n_head, d // self.n_head
+        a = self.attn_norm(x)
+        q = self.q(a).view(B, S, H, dh).transpose(1, 2)
+        k = self.k(a).view(B, S, H, dh).transpose(1, 2)
+        v = self.v(a).view(B, S, H, dh).transpose(1, 2)
+        q, k = _apply_rope(q, cos, sin), _apply_rope(k, cos, sin)
+        att = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+        x = x + self.o(att.transpose(1, 2).reshape(B, S, d))
+        m = self.mlp_norm(x)
+        return x + self.down(F.silu(self.gate(m)) * self.up(m))
+
+
+class LlamaQuartet(torch.nn.Module):
+    """Decoder-only Llama with all linear layers (attention, MLP, LM head) in Quartet MXFP4."""
+
+    def __init__(self, cfg: LlamaConfig, seed: int = 0, device=None, blocks_only: bool = False):
+        super().__init__()
+        self.cfg = cfg
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        self.embed = None if blocks_only else torch.nn.Parameter(
+            (torch.randn(cfg.vocab, cfg.d_model, generator=g) * 0.02).to(device))
+        self.blocks = torch.nn.ModuleList(Block(cfg, i, seed, device) for i in range(cfg.n_layer))
+        self.norm = RMSNorm(cfg.d_model, device=device)
+        self.head = None if blocks_only else QuartetLinear(cfg.d_model, cfg.vocab, seed=seed, layer_id=16 * 4096,
+                                                           rounding=cfg.rounding, device=device)
+        cos, sin = _rope(cfg.seq_len, cfg.d_model // cfg.n_head, cfg.rope_base, device)
+        self.register_buffer("cos", cos, persistent=False)
+        self.register_buffer("sin", sin, persistent=False)
+
+    def forward(self, tokens=None, x=None):
+        if x is None:
+            x = F.embedding(tokens, self.embed).to(torch.bfloat16)
+        for blk in self.blocks:
+            x = blk(x, self.cos, self.sin)
+        if self.head is None:
+            return x
+        return self.head(self.norm(x))
+
+
+def lr_at(step: int, steps: int, lr: float, warmup_frac: float = 0.1, lr_floor: float = 0.0) -> float:
+    """train.py:76-85: linear warm-up to the peak at warmup_frac * steps, then cosine decay."""
+    warmup = max(1, int(round(warmup_frac * steps)))
+    if step < warmup:
+        return lr * (step + 1) / warmup
+    span = max(1, steps - 1 - warmup)
+    t = min(step - warmup, span)
+    return lr_floor + 0.5 * (lr - lr_floor) * (1.0 + math.cos(math.pi * t / span))
+
+
+class GradBucket:
+    """One flat gradient bucket, all-reduced in bf16 (SUM, then / world) -- the data-parallel exchange."""
+
+    def __init__(self, params, comm_dtype=torch.bfloat16):
+        self.params = [p for p in params if p.requires_grad]
+        n = sum(p.numel() for p in self.params)
+        dev = self.params[0].device
+        self.buf = torch.empty(n, dtype=comm_dtype, device=dev)
+
+    def allreduce(self, group=None) -> None:
+        import torch.distributed as dist
+
+        if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+            return
+        world = dist.get_world_size(group)
+        off = 0
+        for p in self.params:
+            n = p.numel()
+            self.buf[off:off + n].copy_(p.grad.reshape(-1))
+            off += n
+        dist.all_reduce(self.buf, group=group)
+        self.buf.div_(world)
+        off = 0
+        for p in self.params:
+            n = p.numel()
+            p.grad.copy_(self.buf[off:off + n].view_as(p.grad))
+            off += n
+
+
+class Trainer:
+    """AdamW / clip / schedule of the reference loop (train.py:325-382) around LlamaQuartet, data parallel."""
+
+    def __init__(self, model: torch.nn.Module, steps: int, lr: float, weight_decay: float = 0.1,
+                 grad_clip: float = 1.0, betas=(0.9, 0.95), eps: float = 1e-8):
+        self.model, self.steps, self.lr, self.grad_clip = model, steps, lr, grad_clip
+        params = [p for p in model.parameters() if p.requires_grad]
+        self.opt = torch.optim.AdamW(params, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay,
+                                     fused=params[0].is_cuda)
+        self.bucket = GradBucket(params)
+        self.step_i = 0
+
+    def step(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        lr = lr_at(self.step_i, self.steps, self.lr)
+        for gr in self.opt.param_groups:
+            gr["lr"] = lr
+        logits = self.model(tokens)
+        loss = F.cross_entropy(logits.view(-1, logits.shape[-1]), targets.reshape(-1))
+        self.opt.zero_grad(set_to_none=False)
+        loss.backward()
+        self.bucket.allreduce()
+        torch.nn.utils.clip_grad_norm_(self.bucket.params, self.grad_clip)
+        self.opt.step()
+        self.step_i += 1
+        return loss.detach()
+
+
+def synthetic_batch(cfg: LlamaConfig, batch: int, seed: int, device) -> tuple[torch.Tensor, torch.Tensor]:
+    """Synthetic token stream of the configured shape (no datasets offline): a noisy periodic sequence
+    so that the loss has structure to learn."""
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    base = torch.randint(0, cfg.vocab, (batch, 1), generator=g)
+    step = torch.randint(1, 97, (batch, 1), generator=g)
+    pos = torch.arange(cfg.seq_len + 1).view(1, -1)
+    seq = (base + step * pos) % cfg.vocab
+    noise = torch.rand(seq.shape, generator=g) < 0.1
+    seq = torch.where(noise, torch.randint(0, cfg.vocab, seq.shape, generator=g), seq)
+    seq = seq.to(device)
+    return seq[:, :-1].contiguous(), seq[:, 1:].contiguous()
