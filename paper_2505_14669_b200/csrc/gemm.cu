@@ -36,6 +36,26 @@ struct GemmSmem {
     static constexpr int TMEM_COLS = BN == 256 ? 512 : 256;
 };
 
+// Grouped tile rasterization: consecutive tile indices walk GROUP_M row blocks before moving to the next
+// column block, so the ~148 tiles in flight share a few A slabs and a few dozen B slabs (L2 reuse instead of
+// re-streaming B from HBM for every row block; e.g. the 4096 x 11008 x 16384 dW GEMM read 1 GB of DRAM
+// with the plain row-major walk).
+// Used for long-K GEMMs (the dW products, K = tokens) where the slabs are large; short-K GEMMs keep the
+// row-major walk (group_m = 0), which measured faster there.
+__device__ __forceinline__ void tile_mn(int tile, int tiles_m, int tiles_n, int& mb, int& nb, int kGroupM = 8) {
+    if (kGroupM == 0) {
+        mb = tile / tiles_n;
+        nb = tile % tiles_n;
+        return;
+    }
+    const int per_group = kGroupM * tiles_n;
+    const int g = tile / per_group, first = g * kGroupM;
+    const int gsize = tiles_m - first < kGroupM ? tiles_m - first : kGroupM;
+    const int r = tile - g * per_group;
+    mb = first + r % gsize;
+    nb = r / gsize;
+}
+
 // Epilogue of one accumulator row slice: columns cbase .. cbase + CW - 1 of output row `row`, held as
 // CW/32 chunks of 32 fp32 values (tcgen05.ld 32x32b); per 64-column pair of chunks (packed f32x2):
 // mask multiply, bit-exact FWHT-32 along N, scale, bf16 / fp32 store.
@@ -118,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int nk = (K + 255) / 256;
-    const int tiles_n = (N + BN - 1) / BN, tiles = ((M + kBM - 1) / kBM) * tiles_n;
+    const int tiles_n = (N + BN - 1) / BN, tiles_m = (M + kBM - 1) / kBM, tiles = tiles_m * tiles_n;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
@@ -142,7 +162,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int it = 0;
             for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-                const int m0 = (tile / tiles_n) * kBM, n0 = (tile % tiles_n) * BN;
+                int mb, nb;
+                tile_mn(tile, tiles_m, tiles_n, mb, nb, K >= 8192 ? 8 : 0);
+                const int m0 = mb * kBM, n0 = nb * BN;
                 for (int kt = 0; kt < nk; ++kt, ++it) {
                     const int s = it % kStages;
                     const uint32_t ph = (it / kStages) & 1;
@@ -227,7 +249,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float2 nz = opaque_nz2();
         int tcount = 0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
-            const int m0 = (tile / tiles_n) * kBM, n0 = (tile % tiles_n) * BN;
+            int mb, nb;
+            tile_mn(tile, tiles_m, tiles_n, mb, nb, K >= 8192 ? 8 : 0);
+            const int m0 = mb * kBM, n0 = nb * BN;
             const int row = m0 + quad * 32 + lane, cbase = n0 + half * CW;
             mbar_wait(tmem_full, tcount & 1);
             tc_fence_after();
@@ -362,7 +386,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int it = 0;
             for (int tile = cid; tile < tiles; tile += ncl) {
-                const int m0 = (tile / tiles_n) * 256 + 128 * rank, n0 = (tile % tiles_n) * BN;
+                int mb, nb;
+                tile_mn(tile, (M + 255) / 256, tiles_n, mb, nb, K >= 8192 ? 8 : 0);
+                const int m0 = mb * 256 + 128 * rank, n0 = nb * BN;
                 for (int kt = 0; kt < nk; ++kt, ++it) {
                     const int s = it % sm2::kStages;
                     mbar_wait(&empty[s], ((it / sm2::kStages) & 1) ^ 1);
@@ -417,7 +443,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint32_t te_leader = mapa_shared(smem_u32(tmem_empty), 0);
         int tcount = 0;
         for (int tile = cid; tile < tiles; tile += ncl, ++tcount) {
-            const int m0 = (tile / tiles_n) * 256 + 128 * rank, n0 = (tile % tiles_n) * BN;
+            int mb, nb;
+            tile_mn(tile, (M + 255) / 256, tiles_n, mb, nb, K >= 8192 ? 8 : 0);
+            const int m0 = mb * 256 + 128 * rank, n0 = nb * BN;
             const int row = m0 + quad * 32 + lane, cbase = n0 + half * CW;
             mbar_wait(tmem_full, tcount & 1);
             tc_fence_after();

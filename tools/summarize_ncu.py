@@ -19,8 +19,8 @@ step = launches[half:]  # second iteration of the 3-shape step
 fam = {}
 for _, name, ns in step:
     key = name.split("(")[0].replace("void ", "")
-    key = "k_gemm_mxf4" if "k_gemm" in key else ("k_quant_tile" if "k_quant_tile" in key else
-                                                   ("k_signs" if "k_signs" in key else "torch/other"))
+    key = ("k_gemm_mxf4" if "k_gemm" in key else "k_tcq_dual" if "k_tcq" in key else
+           "k_quant" if "k_quant" in key else "k_signs" if "k_signs" in key else "torch/other")
     fam[key] = fam.get(key, 0.0) + ns
 total = sum(fam.values())
 with open(f"{out_dir}/{tag}_launch_shares.json", "w") as f:
@@ -32,7 +32,10 @@ with open(f"{out_dir}/{tag}_launch_shares.json", "w") as f:
                "launches": [{"name": n[:90], "us": round(t / 1e3, 2)} for _, n, t in step]}, f, indent=1)
 
 # ---- full capture: per-kernel key metrics
-raw = subprocess.run(["ncu", "-i", f"gpurun_out/full_{tag}.ncu-rep", "--page", "raw", "--csv"], capture_output=True,
+import os
+
+rep_dir = os.environ.get("REP_DIR", "gpurun_out")
+raw = subprocess.run(["ncu", "-i", f"{rep_dir}/full_{tag}.ncu-rep", "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
 H = rr[0]
@@ -80,7 +83,7 @@ for r in rr[2:]:
 gemms = [k for k in kern if "gemm" in k["kernel"]]
 traffic = sum(k.get("dram_read", 0) + k.get("dram_write", 0) for k in gemms) / max(1, len(gemms))
 with open(f"{out_dir}/{tag}_ncu_full_summary.json", "w") as f:
-    json.dump({"source": "ncu --set full --clock-control none -k regex:k_gemm|k_quant -s 21 -c 21 "
+    json.dump({"source": "ncu --set full --clock-control none -k regex:k_gemm|k_quant|k_tcq -s 18 -c 18 "
                          "tools/prof_step.py --all-shapes (one full bench step)", "kernels": kern}, f, indent=1)
 with open(f"{out_dir}/ncu_traffic.json", "w") as f:
     json.dump({"gemm_dram_bytes_per_launch": round(traffic), "launches": len(gemms),
