@@ -1,0 +1,42 @@
+"""End-to-end loss parity on the reference's own teacher-student task.
+
+The reference's toy loop (mx4train/train.py:325-382) is run with every quantized linear layer on the
+B200 path (tests/toy_teacher.py) and compared with the reference's own loss histories, recorded by
+tests/golden/make_teacher_golden.py from the reference itself (seed 0 task, selftest run seeds).
+
+Stated tolerance: the per-layer quantized operands are bit-identical to the reference; only the fp32
+accumulation order inside the tcgen05 GEMMs may differ (at these K <= 128 the FP4 x FP4 x E8M0 products
+and their sums are exact, so in practice nothing differs), and the host-side targets use numpy's BLAS:
+every logged loss and the final held-out loss within 1e-4 relative (observed on B200: 0 to print
+precision, final 0.62613 / 0.62977 = the reference's 0.6261341 / 0.6297728).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "teacher_runs.npz")
+
+
+@pytest.mark.parametrize("pair", ["quest_rtn", "quest_sr"])
+def test_teacher_loss_parity(oracle, pair):
+    import paper_2505_14669_b200 as qt
+    from toy_teacher import Teacher, train
+
+    qt.load()
+    z = np.load(GOLDEN)
+    task = Teacher(oracle, seed=0)
+    fwd, bwd = pair.split("_")
+    s = 0
+    ref_hist, ref_final = z[f"{pair}_s{s}_history"], float(z[f"{pair}_s{s}_final"])
+    hist, final = train(qt, oracle, task, int(z[f"{pair}_s{s}_seed"]), fwd=fwd, bwd=bwd)
+    assert hist.shape == ref_hist.shape
+    assert np.array_equal(hist[:, 0], ref_hist[:, 0])
+    assert np.allclose(hist[:, 2], ref_hist[:, 2], rtol=1e-12)           # identical schedule
+    assert abs(hist[0, 1] / ref_hist[0, 1] - 1) < 1e-4                    # identical first step
+    rel = np.abs(hist[:, 1] / ref_hist[:, 1] - 1)
+    print(f"{pair}: final {final:.9f} vs reference {ref_final:.9f}; max rel dev {rel.max():.3e}")
+    assert rel.max() < 1e-4, rel
+    assert abs(final / ref_final - 1) < 1e-4
