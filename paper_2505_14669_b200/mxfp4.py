@@ -80,8 +80,7 @@ class MXOperand:
         grid = torch.tensor([0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0], dtype=torch.float64, device=self.codes.device)
         dec = torch.cat([grid, -grid])
         vals = dec[self.unpacked_codes().long()]
-        s = torch.ldexp(torch.ones((), dtype=torch.float64, device=self.codes.device),
-                        self.scales_rowmajor().to(torch.int64) - 127)
+        s = torch.exp2(self.scales_rowmajor().to(torch.float64) - 127.0)
         return (vals * s.repeat_interleave(GROUP, dim=1)).to(dtype)
 
 

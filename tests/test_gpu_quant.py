@@ -316,3 +316,22 @@ def test_tensor_core_dual_equals_exact_path(qt, oracle, case):
         gth = oracle.fwht(np.ascontiguousarray(xf.T) * s_r[None, :], 32) * np.float32(0.75)
         c, s = oracle.quantize_rtn(gth.astype(np.float64), 32)
         assert_operand_equal(gt0, c, s, "G_t")
+
+
+def test_mxf4_export_of_gpu_operand_matches_oracle(qt, oracle):
+    """Forward operand quantized on the GPU, exported as the reference's MXF4 container: byte-identical
+    to serializing the oracle's QuantizedTensor (codec.py:214-216)."""
+    import struct
+
+    from paper_2505_14669_b200 import _lib
+    from paper_2505_14669_b200.formats import from_mxf4, to_mxf4, to_msk1
+    from paper_2505_14669_b200.mxfp4 import quant_rows
+
+    x = bf16_values(np.random.default_rng(9).normal(size=(256, 192)).astype(np.float32))
+    op = quant_rows(to_dev(x, torch.bfloat16), _lib.QT_TRANSFORM_HADAMARD, _lib.QT_ROUND_QUEST, want_mask=True)
+    c, s, m = oracle.quantize_quest(oracle.fwht(x, 32).astype(np.float64), 32, 1 / 16)
+    packed = (c[:, 0::2] | (c[:, 1::2] << 4)).astype(np.uint8)
+    assert to_mxf4(op) == struct.pack("<4sHIIHH", b"MXF4", 1, 256, 192, 32, 0) + packed.tobytes() + s.tobytes()
+    assert to_msk1(op)[12:] == np.packbits(m.astype(bool), axis=1, bitorder="little").tobytes()
+    back = from_mxf4(to_mxf4(op))
+    assert torch.equal(back.codes, op.codes) and torch.equal(back.scales_rowmajor(), op.scales_rowmajor())
