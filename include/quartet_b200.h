@@ -174,8 +174,9 @@ QT_API int qt_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_sf, const uint8
 /* Experiment hook for the GEMM mainloop studies in tools/gemm_probe.py (0 = production). */
 QT_API void qt_debug_set_gemm(int dbg);
 /* Quantizer path selection for A/B parity tests: mode 0 (production) uses the tensor-core Hadamard
- * quantizer where eligible, mode 1 forces the CUDA-core path; `fallbacks` (nullable device int) counts
- * groups the tensor-core path re-decided exactly.  Not thread-safe; tests only. */
+ * quantizer for the backward dual operands, mode 1 forces the CUDA-core path everywhere, mode 2 also
+ * routes qt_quant_fused to the (slower, experimental) tensor-core transposed requantization; `fallbacks`
+ * (nullable device int) counts groups a tensor-core path re-decided exactly.  Not thread-safe; tests only. */
 QT_API void qt_debug_set_quant(int mode, int* fallbacks);
 
 #ifdef __cplusplus

@@ -1,0 +1,150 @@
+// tcq.cuh -- shared pieces of the tensor-core Hadamard quantizers (tcq.cu: backward dy operands,
+// tcq_fwd.cu: forward operand + transposed requantization).  See tcq.cu for the error-bound proof.
+#pragma once
+#include "launch.h"
+#include "qgroup.cuh"
+
+namespace qt {
+
+// element (r, c) of a 128 x 128 bf16 tile stored as two TMA SWIZZLE_128B boxes of 64 columns
+__device__ __forceinline__ int tq_off(int r, int c) {
+    return (c >> 6) * 16384 + r * 128 + ((((c & 63) >> 3) ^ (r & 7)) << 4) + ((c & 7) << 1);
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// tcgen05.mma kind::f16 (bf16 x bf16 -> fp32), D[tmem] (+)= A[smem] B[smem]^T
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// instruction descriptor: D f32, A/B bf16, A K-major (a_mn = 0) or MN-major (1), B K-major
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(M >> 4) << 24);
+}
+
+// Checked RTN of one group from tensor-core sums acc (= H (s.x), exact up to 8u sum|x|).
+// Returns false when a decision is within the error bound (caller falls back to the exact path).
+__device__ __forceinline__ bool rtn_checked(const float (&acc)[32], float prescale, uint4& codes, int& e_out) {
+    constexpr float kC5 = 0.17677669f;          // fl(c^5) ~ 2^-2.5 (the tensor-core sum lacks the c^5)
+    constexpr float kU = 5.9604645e-08f;        // 2^-24
+    const float amax = absmax32(acc);
+    // branch-free so that two groups interleave; acc == 0 only for x == 0 (H is invertible and the error
+    // is below |Hx|), which encodes to zero codes with e = 0 like the reference
+    bool ok = amax <= 1.0e30f && (amax >= 1.0e-30f || amax == 0.0f);   // NaN / huge / subnormal -> exact
+    // sum|x| <= ||H x||_2: one FFMA per element buys a ~2x tighter bound than sqrt(32) max|H x|
+    float ss0 = 0.f, ss1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+        ss0 = __fmaf_rn(acc[j], acc[j], ss0);
+        ss1 = __fmaf_rn(acc[j + 1], acc[j + 1], ss1);
+    }
+    const float nrm = __fsqrt_ru(__fadd_ru(ss0, ss1));
+    const float bnd = 20.0f * kU * kC5 * nrm * 1.001f;                 // |y - acc c^5| (y units)
+    const float amp = amax * kC5 * prescale;
+    const float d = bnd * prescale + 4.0f * kU * amp;
+    // E8M0 of the ceil rule (ceil_scale_exp without clamps: 1e-30 <= amax <= 1e30 keeps e in [22, 227]);
+    // the reference's exponent is e iff its absmax lies in (3, 6] * 2^(e-127): check with margin d
+    const uint32_t ab = __float_as_uint(amp);
+    const int e = amax == 0.0f ? 0 : (int)(ab >> 23) - 2 + ((ab & 0x7FFFFFu) > 0x400000u ? 1 : 0);
+    const float s2 = __uint_as_float((uint32_t)(254 - e) << 23);       // 2^(127 - e), normal here
+    ok = ok && (amax == 0.0f || (__fmul_rd(amp - d, s2) > 3.0f && __fmul_ru(amp + d, s2) < 6.0f));
+    const float sc = kC5 * prescale * s2;                               // acc -> scaled value
+    const float bv = (bnd * prescale + 2.0f * kU * amp) * s2 + 1.0e-6f;  // + fma rounding at |v| <= 7
+    uint32_t diff = 0, w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        float lo[8], hi[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            lo[k] = __fmaf_rn(acc[8 * q + k], sc, -bv);
+            hi[k] = __fmaf_rn(acc[8 * q + k], sc, bv);
+        }
+        const uint32_t wl = canon8(e2m1x8(lo[0], lo[1], lo[2], lo[3], lo[4], lo[5], lo[6], lo[7]));
+        w[q] = canon8(e2m1x8(hi[0], hi[1], hi[2], hi[3], hi[4], hi[5], hi[6], hi[7]));
+        diff |= wl ^ w[q];
+    }
+    codes = make_uint4(w[0], w[1], w[2], w[3]);
+    e_out = e;
+    return ok && diff == 0;
+}
+
+// Exact (v3) path for one group of the staged tile: row group (row r, columns 32g..) or column group
+// (column c, rows 32g..), signs from the global bitmaps, FWHT replaying the reference, RTN.
+static __device__ __noinline__ void exact_group(const uint8_t* tile, bool col, int idx, int g, uint32_t sw,
+                                         float prescale, int* err, uint4& codes, int& e_out) {
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const int r = col ? g * 32 + j : idx, c = col ? idx : g * 32 + j;
+        const uint16_t h = *reinterpret_cast<const uint16_t*>(tile + tq_off(r, c));
+        v[j] = __uint_as_float(((uint32_t)h << 16) ^ (((sw >> j) & 1u) << 31));
+    }
+    fwht_full(v);
+    QuantCfg cf{};
+    cf.prescale = prescale;
+    uint32_t mask;
+    e_out = quant_group<kRtn>(v, cf, 0, err, nullptr, codes, mask);
+}
+
+// sign byte -> 8 bf16 +-1.0 (bit i set -> element i negative), 4 KB
+__device__ __forceinline__ void build_sign_lut(uint8_t* lut) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            w[k] = 0x3F803F80u | (((i >> (2 * k)) & 1u) << 15) | (((i >> (2 * k + 1)) & 1u) << 31);
+        reinterpret_cast<uint4*>(lut)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+// 16-byte chunk (n, k8) of a signed 32 x 32 Hadamard block B[n][k] = s_k H[k][n] (K-major, no swizzle:
+// core matrix (n/8, k8) at ((n/8) * 4 + k8) * 128, row n % 8 at 16 B); sgn = the 32 sign bits (bit k).
+__device__ __forceinline__ void store_b_chunk(uint32_t blk_base, const uint8_t* lut, int n, int k8, uint32_t sgn) {
+    // byte m of P = sign pattern of popc(i & m) & 1 over i = 0..7 (Sylvester row pattern)
+    const uint32_t pat = (uint32_t)(0x963C5AF066CCAA00ull >> (8 * (n & 7))) & 0xFFu;
+    const uint32_t byte = pat ^ ((__popc(k8 & (n >> 3)) & 1) ? 0xFFu : 0u) ^ ((sgn >> (8 * k8)) & 0xFFu);
+    const uint4 v = reinterpret_cast<const uint4*>(lut)[byte];
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(blk_base + ((n >> 3) * 4 + k8) * 128 + (n & 7) * 16),
+                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                      CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled_t tq_encode() {
+    static PFN_encodeTiled_t fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+    }
+    return fn;
+}
+
+// [rows, cols] matrix (row stride ld_bytes) as TMA boxes of 128 bytes x 128 rows, 128-byte swizzle
+static int tq_map(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esz, int64_t rows, int64_t cols,
+                  int64_t ld_bytes) {
+    PFN_encodeTiled_t enc = tq_encode();
+    if (!enc) return 1001;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld_bytes};
+    cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 128};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                   CUDA_SUCCESS
+               ? 0
+               : 1002;
+}
+
+}  // namespace qt

@@ -1,0 +1,23 @@
+"""Fused forward quantizer variants (development aid; timings only)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2505_14669_b200 as qt
+from paper_2505_14669_b200 import _lib
+from paper_2505_14669_b200.mxfp4 import quant_fused, quant_rows, sign_bits
+L = qt.load()
+x = torch.randn(16384, 4096, device="cuda").to(torch.bfloat16)
+s = sign_bits(3, 16384, "cuda")
+H, RT, Q, RTN = _lib.QT_TRANSFORM_HADAMARD, _lib.QT_TRANSFORM_RANDOMIZED, _lib.QT_ROUND_QUEST, _lib.QT_ROUND_RTN
+def t(f, n=10):
+    f(); torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(n): f()
+    b.record(); torch.cuda.synchronize()
+    return a.elapsed_time(b) * 1000 / n
+for mode, name in ((2, "tc hybrid"), (2 | 1 << 4, "tc hybrid, col skip"), (0, "cuda-core fused")):
+    L.qt_debug_set_quant(mode, None)
+    print(f"{name:22s} {t(lambda: quant_fused(x, Q, RTN, transform=H, col_transform=RT, col_signs=s)):8.1f} us")
+L.qt_debug_set_quant(0, None)
+print(f"{'rows only (k_quant)':22s} {t(lambda: quant_rows(x, H, Q, want_mask=True)):8.1f} us")
