@@ -208,17 +208,23 @@ def run_ours(args, rank, world, local_rank):
         for i, (x, w, dy) in enumerate(data):
             # the step's backward seed is known at forward time (train.py:346-348), so X_t / W_t come
             # out of the forward read of X / W (qt_quant_fused)
-            y, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False, bwd_xi=xi * 3 + i)
+            # rank r holds tokens [r T, (r + 1) T) of the global batch: global sign / SR offsets make its
+            # operands exact slices of the single-GPU operands (dp.py)
+            y, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False, bwd_xi=xi * 3 + i,
+                                token_offset=rank * T, total_tokens=world * T)
             dx, dw = qt.backward(dy, ctx, xi=xi * 3 + i, dx_dtype=torch.bfloat16, dw_dtype=torch.float32,
-                                 check_finite=False)
+                                 check_finite=False, token_offset=rank * T, total_tokens=world * T)
             if world > 1:  # data parallel: the token-sum of dW is the only exchange (bf16, NCCL)
-                dist.all_reduce(dw.to(torch.bfloat16))
+                buf = dw.to(torch.bfloat16)
+                dist.all_reduce(buf)
+                dw.copy_(buf)
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
     graph = None
-    if not args.no_graph:
+    # world > 1: the step contains NCCL all-reduces; they are launched eagerly rather than captured
+    if not args.no_graph and world == 1:
         # capture one full step (all shapes, fwd + bwd) once; every replay re-executes every kernel
         graph = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
