@@ -160,6 +160,14 @@ int qt_quant_fused(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64
                 col_counter_ld};
     QuantOut ro{row_codes, row_ldc, row_sf, row_katoms, row_mask, err, fallbacks};
     QuantOut co{col_codes, col_ldc, col_sf, col_katoms, nullptr, err, nullptr};
+    if (g_quant_mode == 3 && in_dtype == QT_IN_BF16 && row_rounding == QT_ROUND_QUEST &&
+        row_transform == QT_TRANSFORM_HADAMARD && row_prescale == 1.0f && col_rounding == QT_ROUND_RTN &&
+        col_transform == QT_TRANSFORM_RANDOMIZED) {
+        // X_q and X_t both on the tensor cores (checked QuEST / RTN, exact per-group fallback)
+        int rc3 = launch_tcq_xq(x, ldx, rows, cols, ro, col_sign_bits, col_prescale, co, g_quant_fallbacks,
+                                (cudaStream_t)stream);
+        return rc3 == 1001 || rc3 == 1002 ? QT_ERR_TMA : rc3;
+    }
     if (g_quant_mode == 2 && col_rounding == QT_ROUND_RTN && col_transform == QT_TRANSFORM_RANDOMIZED &&
         row_transform != QT_TRANSFORM_RANDOMIZED) {
         // X_t / W_t on the tensor cores (checked RTN, exact per-group fallback): bit-identical, but measured

@@ -58,6 +58,9 @@ int launch_quant_tile(const void* x, int in_type, int64_t ldx, const MxIn& mx, i
 int launch_tcq_fwd(const void* x, int in_type, int64_t ldx, int64_t R, int64_t C, const QuantCfg& rc,
                    const QuantOut& row_out, const uint32_t* col_sign_bits, float col_prescale, const QuantOut& col_out,
                    int* fallbacks, cudaStream_t st);
+int launch_tcq_xq(const void* x, int64_t ldx, int64_t R, int64_t C, const QuantOut& row_out,
+                  const uint32_t* col_sign_bits, float col_prescale, const QuantOut& col_out, int* fallbacks,
+                  cudaStream_t st);
 extern int g_tcq_dbg;  // experiment knobs of the tensor-core quantizer (0 in production)
 int launch_tcq_dual(const void* x, int64_t ldx, int64_t R, int64_t C, const uint32_t* row_sign_bits,
                     const uint32_t* col_sign_bits, float prescale, const QuantOut& row_out, const QuantOut& col_out,

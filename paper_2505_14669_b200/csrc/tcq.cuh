@@ -108,9 +108,12 @@ __device__ __forceinline__ void store_b_chunk(uint32_t blk_base, const uint8_t* 
     // byte m of P = sign pattern of popc(i & m) & 1 over i = 0..7 (Sylvester row pattern)
     const uint32_t pat = (uint32_t)(0x963C5AF066CCAA00ull >> (8 * (n & 7))) & 0xFFu;
     const uint32_t byte = pat ^ ((__popc(k8 & (n >> 3)) & 1) ? 0xFFu : 0u) ^ ((sgn >> (8 * k8)) & 0xFFu);
-    const uint4 v = reinterpret_cast<const uint4*>(lut)[byte];
+    uint32_t v0, v1, v2, v3;  // explicit shared-window load (lut is a generic pointer into smem)
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                 : "r"(smem_u32(lut) + byte * 16));
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(blk_base + ((n >> 3) * 4 + k8) * 128 + (n & 7) * 16),
-                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 "r"(v0), "r"(v1), "r"(v2), "r"(v3)
                  : "memory");
 }
 
