@@ -155,6 +155,13 @@ __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// one lane of the (fully active) warp: for issuing single-thread async ops from warp-uniform code
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile("{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n selp.u32 %0, 1, 0, e;\n}" : "=r"(p));
+    return p != 0;
+}
+
 // ----------------------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");

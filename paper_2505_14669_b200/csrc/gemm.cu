@@ -186,65 +186,79 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // Scale factors: the tcgen05.cp of k-tile it + 1 is issued right AFTER the MMAs of k-tile it, into
-            // TMEM set (it + 1) % 4, so a copy's latency overlaps a k-tile of MMAs instead of sitting between the
-            // copy and its dependent MMAs (measured 14-18 % faster than copy-then-MMA on the same k-tile, whose
-            // RAW wait was the mainloop's largest stall).  The commit of k-tile it covers the copy of k-tile it
-            // (issued one k-tile earlier), so no stage is released before its scale bytes are in TMEM; reusing a
-            // set four k-tiles later is ordered behind the MMAs that read it (tcgen05 ops issue in order).
-            // dbg bit 0 (timing only): no copies after the first k-tile of each tile.
-            auto sf_copy = [&](int itx, int set) {
-                const int sx = itx % kStages;
-                const uint32_t a_sf = smem_u32(sSFA + sx * L::SFA), b_sf = smem_u32(sSFB + sx * L::SFB);
-                const uint32_t ta = t_sfa + set * 32, tb = t_sfb + set * 32;
-                tmem_cp_sf(ta + 0, make_sdesc(a_sf, 0, 128, kLayoutNone));
-                tmem_cp_sf(ta + 4, make_sdesc(a_sf + 512, 0, 128, kLayoutNone));
+        // The whole warp walks the issue loop (warp-uniform control flow keeps every operand in uniform
+        // registers) and one elected lane issues each tcgen05 op.  The single issuing thread was the
+        // mainloop's limiter (~200 instructions per K tile, waterfall loops around every tcgen05 op), so
+        // descriptors are precomputed once and advanced by adds.
+        //
+        // Scale factors: the tcgen05.cp of k-tile it + 1 is issued right AFTER the MMAs of k-tile it, into
+        // TMEM set (it + 1) % 4, so a copy's latency overlaps a k-tile of MMAs instead of sitting between the
+        // copy and its dependent MMAs (measured 14-18 % faster than copy-then-MMA on the same k-tile).  The
+        // commit of k-tile it covers the copy of k-tile it (issued one k-tile earlier), so no stage is
+        // released before its scale bytes are in TMEM; reusing a set four k-tiles later is ordered behind the
+        // MMAs that read it (tcgen05 ops issue in order).  dbg bit 0 (timing only): no copies after the first
+        // k-tile of each tile.
+        const uint64_t da0 = make_sdesc(smem_u32(sA), 0, 1024, kLayoutSW128);
+        const uint64_t db0 = make_sdesc(smem_u32(sB), 0, 1024, kLayoutSW128);
+        const uint64_t dsa0 = make_sdesc(smem_u32(sSFA), 0, 128, kLayoutNone);
+        const uint64_t dsb0 = make_sdesc(smem_u32(sSFB), 0, 128, kLayoutNone);
+        constexpr uint32_t kStA = L::A >> 4, kStB = L::B >> 4, kStSA = L::SFA >> 4, kStSB = L::SFB >> 4;
+        const uint32_t id0 = idesc_mxf4(kBM, BN, 0, 0), id2 = idesc_mxf4(kBM, BN, 2, 2);
+        const bool no_sf = (ep.dbg & 1) != 0;
+        const int nmma = (ep.dbg & 4) ? 1 : 4;
+        auto sf_copy = [&](uint32_t sx, uint32_t set) {
+            const uint64_t a_sf = dsa0 + sx * kStSA, b_sf = dsb0 + sx * kStSB;
+            const uint32_t ta = t_sfa + set * 32, tb = t_sfb + set * 32;
+            if (elect_one()) {
+                tmem_cp_sf(ta + 0, a_sf);
+                tmem_cp_sf(ta + 4, a_sf + (512 >> 4));
 #pragma unroll
                 for (int rb = 0; rb < BN / 128; ++rb) {
-                    tmem_cp_sf(tb + rb * 4, make_sdesc(b_sf + rb * 1024, 0, 128, kLayoutNone));
-                    tmem_cp_sf(tb + (BN / 128) * 4 + rb * 4, make_sdesc(b_sf + rb * 1024 + 512, 0, 128, kLayoutNone));
+                    tmem_cp_sf(tb + rb * 4, b_sf + rb * (1024 >> 4));
+                    tmem_cp_sf(tb + (BN / 128) * 4 + rb * 4, b_sf + (rb * 1024 + 512 >> 4));
                 }
-            };
-            const bool no_sf = (ep.dbg & 1) != 0;
-            const int my_tiles = tiles > (int)blockIdx.x ? (tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-            const int total = my_tiles * nk;
-            int it = 0, tcount = 0;
-            if (total > 0) {
-                mbar_wait(&full[0], 0);
-                tc_fence_after();
-                sf_copy(0, 0);
             }
-            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
-                mbar_wait(tmem_empty, (tcount & 1) ^ 1);  // epilogue has drained the accumulator
-                tc_fence_after();
-                for (int kt = 0; kt < nk; ++kt, ++it) {
-                    const int s = it % kStages;
-                    mbar_wait(&full[s], (it / kStages) & 1);
-                    tc_fence_after();
-                    const uint32_t a_base = smem_u32(sA + s * L::A), b_base = smem_u32(sB + s * L::B);
-                    const uint32_t so = (no_sf ? 0 : (it & 3)) * 32;
-                    const uint32_t ta = t_sfa + so, tb = t_sfb + so;
-                    const int nmma = (ep.dbg & 4) ? 1 : 4;
+            __syncwarp();
+        };
+        const int my_tiles = tiles > (int)blockIdx.x ? (tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+        const int total = my_tiles * nk;
+        // stage / phase of k-tile `it`, advanced incrementally; full[s] of k-tile it is waited for (and its
+        // scale factors copied) at the end of iteration it - 1
+        uint32_t s = 0, ph = 0;
+        int it = 0;
+        if (total > 0) {
+            mbar_wait(&full[0], 0);
+            tc_fence_after();
+            sf_copy(0, 0);
+        }
+        for (int tcount = 0; tcount < my_tiles; ++tcount) {
+            mbar_wait(tmem_empty, (tcount & 1) ^ 1);  // epilogue has drained the accumulator
+            tc_fence_after();
+            for (int kt = 0; kt < nk; ++kt, ++it) {
+                const uint64_t ad = da0 + s * kStA, bd = db0 + s * kStB;
+                const uint32_t so = (no_sf ? 0u : (uint32_t)(it & 3)) * 32;
+                const uint32_t ta = t_sfa + so, tb = t_sfb + so;
+                if (elect_one()) {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         if (j >= nmma) break;
-                        const uint64_t ad = make_sdesc(a_base + j * 32, 0, 1024, kLayoutSW128);
-                        const uint64_t bd = make_sdesc(b_base + j * 32, 0, 1024, kLayoutSW128);
-                        const uint32_t id = idesc_mxf4(kBM, BN, (j & 1) * 2, (j & 1) * 2);
-                        mma_mxf4(t_acc, ad, bd, id, ta + (j >> 1) * 4, tb + (j >> 1) * (BN / 128) * 4,
-                                 (kt | j) != 0 ? 1u : 0u);
+                        // K step j: 64 E2M1 = 32 bytes into the 128-byte swizzled rows (+2 in the address field)
+                        mma_mxf4(t_acc, ad + 2 * j, bd + 2 * j, (j & 1) ? id2 : id0, ta + (j >> 1) * 4,
+                                 tb + (j >> 1) * (BN / 128) * 4, (kt | j) != 0 ? 1u : 0u);
                     }
                     tc_commit(&empty[s]);
-                    const int nx = it + 1;
-                    if (nx < total && !(no_sf && nx % nk != 0)) {
-                        mbar_wait(&full[nx % kStages], (nx / kStages) & 1);
-                        tc_fence_after();
-                        sf_copy(nx, no_sf ? 0 : (nx & 3));
-                    }
                 }
-                tc_commit(tmem_full);
+                __syncwarp();
+                s = s + 1 == kStages ? 0u : s + 1;
+                ph ^= s == 0 ? 1u : 0u;
+                if (it + 1 < total) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    if (!no_sf || kt + 1 == nk) sf_copy(s, no_sf ? 0u : (uint32_t)((it + 1) & 3));
+                }
             }
+            if (elect_one()) tc_commit(tmem_full);
+            __syncwarp();
         }
     } else {
         // epilogue warps 2..9: TMEM lane quadrant warp % 4, column half (warp - 2) / 4
