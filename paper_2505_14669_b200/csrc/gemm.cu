@@ -159,30 +159,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t t_acc = tmem, t_sfa = tmem + BN, t_sfb = tmem + BN + 8;
 
     if (warp == 0) {
-        if (lane == 0) {
-            int it = 0;
-            for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-                int mb, nb;
-                tile_mn(tile, tiles_m, tiles_n, mb, nb, K >= 8192 ? 8 : 0);
-                const int m0 = mb * kBM, n0 = nb * BN;
-                for (int kt = 0; kt < nk; ++kt, ++it) {
-                    const int s = it % kStages;
-                    const uint32_t ph = (it / kStages) & 1;
-                    mbar_wait(&empty[s], ph ^ 1);
-                    const bool skip_sf = (ep.dbg & 2) && kt > 0;
-                    const bool skip_b = (ep.dbg & 8) && kt > 0;
+        // TMA producer: like the MMA issuer, the whole warp walks the loop (uniform operands) and one elected
+        // lane issues the copies
+        uint32_t s = 0, ph = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+            int mb, nb;
+            tile_mn(tile, tiles_m, tiles_n, mb, nb, K >= 8192 ? 8 : 0);
+            const int m0 = mb * kBM, n0 = nb * BN;
+            const uint8_t* sfa_t = sfa + (int64_t)(m0 / 128) * a_katoms * 512;
+            const uint8_t* sfb_t = sfb + (int64_t)(n0 / 128) * b_katoms * 512;
+            for (int kt = 0; kt < nk; ++kt) {
+                mbar_wait(&empty[s], ph ^ 1);
+                const bool skip_sf = (ep.dbg & 2) && kt > 0;
+                const bool skip_b = (ep.dbg & 8) && kt > 0;
+                if (elect_one()) {
                     mbar_arrive_expect_tx(&full[s], L::STAGE - (skip_sf ? L::SFA + L::SFB : 0) - (skip_b ? L::B : 0));
                     tma_load_2d(sA + s * L::A, &tmA, &full[s], kt * kBKBytes, m0);
                     if (!skip_b) tma_load_2d(sB + s * L::B, &tmB, &full[s], kt * kBKBytes, n0);
                     if (!skip_sf) {
-                        bulk_load(sSFA + s * L::SFA, sfa + ((int64_t)(m0 / 128) * a_katoms + 2 * kt) * 512, 1024,
-                                  &full[s]);
+                        bulk_load(sSFA + s * L::SFA, sfa_t + kt * 1024, 1024, &full[s]);
 #pragma unroll
                         for (int rb = 0; rb < BN / 128; ++rb)
-                            bulk_load(sSFB + s * L::SFB + rb * 1024,
-                                      sfb + ((int64_t)(n0 / 128 + rb) * b_katoms + 2 * kt) * 512, 1024, &full[s]);
+                            bulk_load(sSFB + s * L::SFB + rb * 1024, sfb_t + (int64_t)rb * b_katoms * 512 + kt * 1024,
+                                      1024, &full[s]);
                     }
                 }
+                __syncwarp();
+                s = s + 1 == kStages ? 0u : s + 1;
+                ph ^= s == 0 ? 1u : 0u;
             }
         }
     } else if (warp == 1) {
