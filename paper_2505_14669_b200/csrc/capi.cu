@@ -17,7 +17,7 @@ extern "C" {
 
 void qt_debug_set_gemm(int dbg) {
     g_gemm_dbg = dbg & 0xFFFF;
-    qt::g_gemm_2sm = (dbg & 0x20000) ? 1 : 0;  // bit 17: use the 2-CTA kernel
+    qt::g_gemm_2sm = (dbg & 0x40000) ? 0 : 1;  // bit 18: force the 1-CTA kernel (A/B tests)
 }
 
 void qt_debug_set_quant(int mode, int* fallbacks) {

@@ -404,15 +404,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t t_acc = tmem, t_sfa = tmem + BN, t_sfb = tmem + BN + 8;
 
     if (warp == 0) {
-        if (lane == 0) {
-            int it = 0;
-            for (int tile = cid; tile < tiles; tile += ncl) {
-                int mb, nb;
-                tile_mn(tile, (M + 255) / 256, tiles_n, mb, nb, K >= 8192 ? 8 : 0);
-                const int m0 = mb * 256 + 128 * rank, n0 = nb * BN;
-                for (int kt = 0; kt < nk; ++kt, ++it) {
-                    const int s = it % sm2::kStages;
-                    mbar_wait(&empty[s], ((it / sm2::kStages) & 1) ^ 1);
+        // producer (warp-uniform loop, elected issue): this CTA's A half and B half, its A scale atoms and all
+        // 256 B rows' atoms, completing on the leader's full barrier
+        uint32_t s = 0, ph = 0;
+        for (int tile = cid; tile < tiles; tile += ncl) {
+            int mb, nb;
+            tile_mn(tile, (M + 255) / 256, tiles_n, mb, nb, K >= 8192 ? 8 : 0);
+            const int m0 = mb * 256 + 128 * rank, n0 = nb * BN;
+            for (int kt = 0; kt < nk; ++kt) {
+                mbar_wait(&empty[s], ph ^ 1);
+                if (elect_one()) {
                     const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
                     if (leader) mbar_arrive_expect_tx(&full[s], 2 * sm2::kStage);
                     tma_load_2d_2sm(sA + s * sm2::kA, &tmA, fb, kt * kBKBytes, m0);
@@ -421,41 +422,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     tma_load_2d_2sm(sSFA + s * sm2::kSFA, &tmSFA, fb, kt * 256, m0 / 128);
                     tma_load_2d_2sm(sSFB + s * sm2::kSFB, &tmSFB, fb, kt * 256, n0 / 128);
                 }
+                __syncwarp();
+                s = s + 1 == sm2::kStages ? 0u : s + 1;
+                ph ^= s == 0 ? 1u : 0u;
             }
         }
     } else if (warp == 1) {
-        if (leader && lane == 0) {
-            int it = 0, tcount = 0;
-            for (int tile = cid; tile < tiles; tile += ncl, ++tcount) {
+        if (leader) {
+            // issue loop as in k_gemm_mxf4 (warp-uniform, elected issue, scale copies one k-tile ahead into
+            // rotating TMEM sets); cta_group::2 MMAs and copies act on both CTAs of the pair
+            const uint64_t da0 = make_sdesc(smem_u32(sA), 0, 1024, kLayoutSW128);
+            const uint64_t db0 = make_sdesc(smem_u32(sB), 0, 1024, kLayoutSW128);
+            const uint64_t dsa0 = make_sdesc(smem_u32(sSFA), 0, 128, kLayoutNone);
+            const uint64_t dsb0 = make_sdesc(smem_u32(sSFB), 0, 128, kLayoutNone);
+            const uint32_t id0 = idesc_mxf4(256, BN, 0, 0), id2 = idesc_mxf4(256, BN, 2, 2);
+            auto sf_copy = [&](uint32_t sx, uint32_t set) {
+                const uint64_t a_sf = dsa0 + sx * (sm2::kSFA >> 4), b_sf = dsb0 + sx * (sm2::kSFB >> 4);
+                const uint32_t ta = t_sfa + set * 32, tb = t_sfb + set * 32;
+                if (elect_one()) {
+                    tmem_cp_sf_2sm(ta + 0, a_sf);
+                    tmem_cp_sf_2sm(ta + 4, a_sf + (512 >> 4));
+#pragma unroll
+                    for (int rb = 0; rb < 2; ++rb) {
+                        tmem_cp_sf_2sm(tb + rb * 4, b_sf + rb * (1024 >> 4));
+                        tmem_cp_sf_2sm(tb + 8 + rb * 4, b_sf + (rb * 1024 + 512 >> 4));
+                    }
+                }
+                __syncwarp();
+            };
+            const int my_tiles = tiles > cid ? (tiles - 1 - cid) / ncl + 1 : 0;
+            const int total = my_tiles * nk;
+            uint32_t s = 0, ph = 0;
+            int it = 0;
+            if (total > 0) {
+                mbar_wait(&full[0], 0);
+                tc_fence_after();
+                sf_copy(0, 0);
+            }
+            for (int tcount = 0; tcount < my_tiles; ++tcount) {
                 mbar_wait(tmem_empty, (tcount & 1) ^ 1);  // both CTAs' epilogues drained the accumulator
                 tc_fence_after();
                 for (int kt = 0; kt < nk; ++kt, ++it) {
-                    const int s = it % sm2::kStages;
-                    mbar_wait(&full[s], (it / sm2::kStages) & 1);
-                    tc_fence_after();
-                    const uint32_t a_sf = smem_u32(sSFA + s * sm2::kSFA), b_sf = smem_u32(sSFB + s * sm2::kSFB);
-                    if (!((ep.dbg & 1) && kt > 0)) {
-                    tmem_cp_sf_2sm(t_sfa + 0, make_sdesc(a_sf, 0, 128, kLayoutNone));
-                    tmem_cp_sf_2sm(t_sfa + 4, make_sdesc(a_sf + 512, 0, 128, kLayoutNone));
+                    const uint64_t ad = da0 + s * (sm2::kA >> 4), bd = db0 + s * (sm2::kB >> 4);
+                    const uint32_t so = (uint32_t)(it & 3) * 32;
+                    if (elect_one()) {
 #pragma unroll
-                    for (int rb = 0; rb < 2; ++rb) {
-                        tmem_cp_sf_2sm(t_sfb + rb * 4, make_sdesc(b_sf + rb * 1024, 0, 128, kLayoutNone));
-                        tmem_cp_sf_2sm(t_sfb + 8 + rb * 4, make_sdesc(b_sf + rb * 1024 + 512, 0, 128, kLayoutNone));
+                        for (int j = 0; j < 4; ++j)
+                            mma_mxf4_2sm(t_acc, ad + 2 * j, bd + 2 * j, (j & 1) ? id2 : id0, t_sfa + so + (j >> 1) * 4,
+                                         t_sfb + so + (j >> 1) * 8, (kt | j) != 0 ? 1u : 0u);
+                        tc_commit_2sm(&empty[s]);
                     }
+                    __syncwarp();
+                    s = s + 1 == sm2::kStages ? 0u : s + 1;
+                    ph ^= s == 0 ? 1u : 0u;
+                    if (it + 1 < total) {
+                        mbar_wait(&full[s], ph);
+                        tc_fence_after();
+                        sf_copy(s, (uint32_t)((it + 1) & 3));
                     }
-                    const uint32_t a_base = smem_u32(sA + s * sm2::kA), b_base = smem_u32(sB + s * sm2::kB);
-                    const int nmma = (ep.dbg & 4) ? 1 : 4;
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        if (j >= nmma) break;
-                        const uint64_t ad = make_sdesc(a_base + j * 32, 0, 1024, kLayoutSW128);
-                        const uint64_t bd = make_sdesc(b_base + j * 32, 0, 1024, kLayoutSW128);
-                        mma_mxf4_2sm(t_acc, ad, bd, idesc_mxf4(256, BN, (j & 1) * 2, (j & 1) * 2),
-                                     t_sfa + (j >> 1) * 4, t_sfb + (j >> 1) * 8, (kt | j) != 0 ? 1u : 0u);
-                    }
-                    tc_commit_2sm(&empty[s]);
                 }
-                tc_commit_2sm(tmem_full);
+                if (elect_one()) tc_commit_2sm(tmem_full);
+                __syncwarp();
             }
         }
     } else {
@@ -491,7 +518,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------- host side
-int g_gemm_2sm = 0;  // 1: use the 2-CTA kernel where eligible (measured no faster yet: see DESIGN.md)
+int g_gemm_2sm = 1;  // use the 2-CTA kernel where eligible (N % 256 == 0, M >= 256); 0: 1-CTA kernel only
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,

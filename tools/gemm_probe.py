@@ -18,7 +18,7 @@ for (M, N, K) in [(16384, 4096, 4096), (16384, 4096, 16384)]:
     A = qt.quant_rows(x, 0, _lib.QT_ROUND_RTN)
     B = qt.quant_rows(w, 0, _lib.QT_ROUND_RTN)
     out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
-    for dbg, name in [(0, "baseline"), (1, "no SF tcgen05.cp after k0"), (3, "no SF loads+cp after k0"),
+    for dbg, name in [(0, "baseline (2-CTA pairs)"), (0x40000, "1-CTA 128x256 tiles"), (1, "no SF tcgen05.cp after k0"), (3, "no SF loads+cp after k0"),
                       (4, "1 MMA per k-tile (1/4 math)"), (8, "no B TMA after k0"), (12, "no B + 1 MMA"),
                       (11, "no B, no SF")]:
         L.qt_debug_set_gemm(dbg)
