@@ -436,10 +436,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t dsa0 = make_sdesc(smem_u32(sSFA), 0, 128, kLayoutNone);
             const uint64_t dsb0 = make_sdesc(smem_u32(sSFB), 0, 128, kLayoutNone);
             const uint32_t id0 = idesc_mxf4(256, BN, 0, 0), id2 = idesc_mxf4(256, BN, 2, 2);
-            auto sf_copy = [&](uint32_t sx, uint32_t set) {
-                const uint64_t a_sf = dsa0 + sx * (sm2::kSFA >> 4), b_sf = dsb0 + sx * (sm2::kSFB >> 4);
-                const uint32_t ta = t_sfa + set * 32, tb = t_sfb + set * 32;
-                if (elect_one()) {
+            const int my_tiles = tiles > cid ? (tiles - 1 - cid) / ncl + 1 : 0;
+            const int total = my_tiles * nk;
+            // one elected lane walks the whole issue loop: a single divergence region, every loop value uniform
+            if (elect_one()) {
+                auto sf_copy = [&](uint32_t sx, uint32_t set) {
+                    const uint64_t a_sf = dsa0 + sx * (sm2::kSFA >> 4), b_sf = dsb0 + sx * (sm2::kSFB >> 4);
+                    const uint32_t ta = t_sfa + set * 32, tb = t_sfb + set * 32;
                     tmem_cp_sf_2sm(ta + 0, a_sf);
                     tmem_cp_sf_2sm(ta + 4, a_sf + (512 >> 4));
 #pragma unroll
@@ -447,43 +450,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         tmem_cp_sf_2sm(tb + rb * 4, b_sf + rb * (1024 >> 4));
                         tmem_cp_sf_2sm(tb + 8 + rb * 4, b_sf + (rb * 1024 + 512 >> 4));
                     }
+                };
+                uint32_t s = 0, ph = 0;
+                int it = 0;
+                if (total > 0) {
+                    mbar_wait(&full[0], 0);
+                    tc_fence_after();
+                    sf_copy(0, 0);
                 }
-                __syncwarp();
-            };
-            const int my_tiles = tiles > cid ? (tiles - 1 - cid) / ncl + 1 : 0;
-            const int total = my_tiles * nk;
-            uint32_t s = 0, ph = 0;
-            int it = 0;
-            if (total > 0) {
-                mbar_wait(&full[0], 0);
-                tc_fence_after();
-                sf_copy(0, 0);
-            }
-            for (int tcount = 0; tcount < my_tiles; ++tcount) {
-                mbar_wait(tmem_empty, (tcount & 1) ^ 1);  // both CTAs' epilogues drained the accumulator
-                tc_fence_after();
-                for (int kt = 0; kt < nk; ++kt, ++it) {
-                    const uint64_t ad = da0 + s * (sm2::kA >> 4), bd = db0 + s * (sm2::kB >> 4);
-                    const uint32_t so = (uint32_t)(it & 3) * 32;
-                    if (elect_one()) {
+                for (int tcount = 0; tcount < my_tiles; ++tcount) {
+                    mbar_wait(tmem_empty, (tcount & 1) ^ 1);  // both CTAs' epilogues drained the accumulator
+                    tc_fence_after();
+                    for (int kt = 0; kt < nk; ++kt, ++it) {
+                        const uint64_t ad = da0 + s * (sm2::kA >> 4), bd = db0 + s * (sm2::kB >> 4);
+                        const uint32_t so = (uint32_t)(it & 3) * 32;
 #pragma unroll
                         for (int j = 0; j < 4; ++j)
                             mma_mxf4_2sm(t_acc, ad + 2 * j, bd + 2 * j, (j & 1) ? id2 : id0, t_sfa + so + (j >> 1) * 4,
                                          t_sfb + so + (j >> 1) * 8, (kt | j) != 0 ? 1u : 0u);
                         tc_commit_2sm(&empty[s]);
+                        s = s + 1 == sm2::kStages ? 0u : s + 1;
+                        ph ^= s == 0 ? 1u : 0u;
+                        if (it + 1 < total) {
+                            mbar_wait(&full[s], ph);
+                            tc_fence_after();
+                            sf_copy(s, (uint32_t)((it + 1) & 3));
+                        }
                     }
-                    __syncwarp();
-                    s = s + 1 == sm2::kStages ? 0u : s + 1;
-                    ph ^= s == 0 ? 1u : 0u;
-                    if (it + 1 < total) {
-                        mbar_wait(&full[s], ph);
-                        tc_fence_after();
-                        sf_copy(s, (uint32_t)((it + 1) & 3));
-                    }
+                    tc_commit_2sm(tmem_full);
                 }
-                if (elect_one()) tc_commit_2sm(tmem_full);
-                __syncwarp();
             }
+            __syncwarp();
         }
     } else {
         const int quad = warp % 4, half = (warp - 2) / 4;
@@ -505,7 +502,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(te_leader);  // the leader may start the next tile
-            if (row >= M) continue;
+            if (row >= M || (ep.dbg & 0x100)) continue;   // dbg 0x100 (timing only): no epilogue math/stores
             epi_store<CW>(acc, row, cbase, N, ep, nz);
         }
     }
