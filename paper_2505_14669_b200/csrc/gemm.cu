@@ -304,14 +304,96 @@ __global__ void __launch_bounds__(kThreads, 1)
 // leader (rank 0) issues MMAs and scale-factor copies (cta_group::2 acts on both CTAs); both CTAs'
 // TMA loads complete on the leader's full barrier, MMA commits multicast to both CTAs' barriers.
 namespace sm2 {
-constexpr int kStages = 6;
+constexpr int kStages = 5;
 constexpr int kA = 128 * kBKBytes;     // own 128 A rows
 constexpr int kB = 128 * kBKBytes;     // own 128 of the 256 B rows
 constexpr int kSFA = 1024;             // own 128 rows x 8 groups
 constexpr int kSFB = 2048;             // all 256 B rows x 8 groups
 constexpr int kStage = kA + kB + kSFA + kSFB;
-constexpr int kBytes = kStages * kStage + 1024 + 256;
+constexpr int kBox = 128 * 128;        // output staging box: 128 rows x 128 bytes (64 bf16 / 32 fp32 columns)
+constexpr int kBytes = kStages * kStage + 2 * kBox + 1024 + 256;
 }  // namespace sm2
+
+// Staged epilogue of one accumulator row slice for the 2-CTA kernel: per 64-column pair the values are
+// computed as in epi_store, written to a 128-row x 128-byte shared-memory box (SWIZZLE_128B layout, the
+// 16-byte chunk k of row r at (k ^ r % 8)) and stored by TMA (full lines, asynchronous, rows/columns past
+// M/N clipped by the tensor map).  The 4 warps of a column half share a box: named barrier 1 + half.
+__device__ __forceinline__ void fence_proxy_async_cta() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(x), "r"(y)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <int CW>
+__device__ __forceinline__ void epi_stage(const uint32_t (&acc)[CW / 32][32], int row, int r_box, int cbase, int M,
+                                          const EpiParams& ep, float2 nz, const CUtensorMap* tmO, uint8_t* box,
+                                          int half, bool issuer, int y0) {
+    const bool live = row < M;
+#pragma unroll
+    for (int pj = 0; pj < CW / 64; ++pj) {
+        const int col0 = cbase + pj * 64;
+        Pair g;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            g.p[i] = make_float2(__uint_as_float(acc[2 * pj][i]), __uint_as_float(acc[2 * pj + 1][i]));
+        if (ep.mode != kEpiStore) {
+            const uint32_t mA = live ? __ldg(ep.mask + (int64_t)row * ep.ldm + col0 / 32) : 0u;
+            const uint32_t mB = live ? __ldg(ep.mask + (int64_t)row * ep.ldm + col0 / 32 + 1) : 0u;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                g.p[i].x = ((mA >> i) & 1u) ? g.p[i].x : 0.0f;
+                g.p[i].y = ((mB >> i) & 1u) ? g.p[i].y : 0.0f;
+            }
+            if (ep.mode == kEpiMaskH) fwht_pair(g, nz);
+            scale_pair(g, ep.scale);
+        }
+        uint8_t* rowp = box + r_box * 128;
+        const int sw = r_box & 7;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            // bf16: one box holds both 32-column chunks; fp32: one box per chunk
+            if (ep.out_bf16 ? (h == 0) : true) {
+                if (issuer) bulk_wait_read0();  // the previous store out of this box has read it
+                named_bar(1 + half, 128);
+            }
+            if (ep.out_bf16) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int i = q * 8 + 2 * t;
+                        __nv_bfloat162 b2 = h ? __floats2bfloat162_rn(g.p[i].y, g.p[i + 1].y)
+                                              : __floats2bfloat162_rn(g.p[i].x, g.p[i + 1].x);
+                        w[t] = *reinterpret_cast<uint32_t*>(&b2);
+                    }
+                    *reinterpret_cast<uint4*>(rowp + (((h * 4 + q) ^ sw) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int i = 4 * q;
+                    *reinterpret_cast<float4*>(rowp + ((q ^ sw) << 4)) =
+                        h ? make_float4(g.p[i].y, g.p[i + 1].y, g.p[i + 2].y, g.p[i + 3].y)
+                          : make_float4(g.p[i].x, g.p[i + 1].x, g.p[i + 2].x, g.p[i + 3].x);
+                }
+            }
+            if (ep.out_bf16 ? (h == 1) : true) {
+                fence_proxy_async_cta();
+                named_bar(1 + half, 128);
+                if (issuer) {
+                    tma_store_2d(tmO, box, ep.out_bf16 ? col0 : col0 + 32 * h, y0);
+                    bulk_commit();
+                }
+            }
+        }
+    }
+}
 
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -357,8 +439,8 @@ __device__ __forceinline__ void tc_commit_2sm(uint64_t* bar) {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     k_gemm_mxf4_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB, int M, int N,
-                    int K, EpiParams ep) {
+                    const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
+                    const __grid_constant__ CUtensorMap tmO, int M, int N, int K, EpiParams ep) {
     constexpr int BN = 256, CW = BN / 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -366,7 +448,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint8_t* sB = sA + sm2::kStages * sm2::kA;
     uint8_t* sSFA = sB + sm2::kStages * sm2::kB;
     uint8_t* sSFB = sSFA + sm2::kStages * sm2::kSFA;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sSFB + sm2::kStages * sm2::kSFB);
+    uint8_t* sBox = sSFB + sm2::kStages * sm2::kSFB;  // 2 output staging boxes (one per column half)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sBox + 2 * sm2::kBox);
     uint64_t* empty = full + sm2::kStages;
     uint64_t* tmem_full = empty + sm2::kStages;
     uint64_t* tmem_empty = tmem_full + 1;
@@ -378,6 +461,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int nk = (K + 255) / 256;
     const int tiles_n = (N + BN - 1) / BN, tiles = ((M + 255) / 256) * tiles_n;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    // tile walk: grouped (gm row blocks per column sweep) for long K, row-major otherwise; dbg 0x1000 / 0x2000
+    // force grouped-4 / grouped-16 (timing experiments)
+    const int gm = (ep.dbg & 0x1000) ? 4 : (ep.dbg & 0x2000) ? 16 : (ep.dbg & 0x4000) ? 2 : (K >= 8192 ? 8 : 0);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
@@ -409,7 +495,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t s = 0, ph = 0;
         for (int tile = cid; tile < tiles; tile += ncl) {
             int mb, nb;
-            tile_mn(tile, (M + 255) / 256, tiles_n, mb, nb, K >= 8192 ? 8 : 0);
+            tile_mn(tile, (M + 255) / 256, tiles_n, mb, nb, gm);
             const int m0 = mb * 256 + 128 * rank, n0 = nb * BN;
             for (int kt = 0; kt < nk; ++kt) {
                 mbar_wait(&empty[s], ph ^ 1);
@@ -484,12 +570,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
     } else {
         const int quad = warp % 4, half = (warp - 2) / 4;
+        const bool issuer = ((warp - 2) & 3) == 0 && lane == 0;  // one thread per column half issues the stores
         const float2 nz = opaque_nz2();
         const uint32_t te_leader = mapa_shared(smem_u32(tmem_empty), 0);
+        uint8_t* box = sBox + half * sm2::kBox;
         int tcount = 0;
         for (int tile = cid; tile < tiles; tile += ncl, ++tcount) {
             int mb, nb;
-            tile_mn(tile, (M + 255) / 256, tiles_n, mb, nb, K >= 8192 ? 8 : 0);
+            tile_mn(tile, (M + 255) / 256, tiles_n, mb, nb, gm);
             const int m0 = mb * 256 + 128 * rank, n0 = nb * BN;
             const int row = m0 + quad * 32 + lane, cbase = n0 + half * CW;
             mbar_wait(tmem_full, tcount & 1);
@@ -502,9 +590,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(te_leader);  // the leader may start the next tile
-            if (row >= M || (ep.dbg & 0x100)) continue;   // dbg 0x100 (timing only): no epilogue math/stores
-            epi_store<CW>(acc, row, cbase, N, ep, nz);
+            if (ep.dbg & 0x100) continue;                   // timing only: no epilogue math/stores
+            epi_stage<CW>(acc, row, quad * 32 + lane, cbase, M, ep, nz, &tmO, box, half, issuer, m0);
         }
+        if (issuer) bulk_wait0();
     }
     tc_fence_before();
     cluster_sync_all();
@@ -596,6 +685,20 @@ static int launch_gemm_2sm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, i
     if (!rc) rc = make_sf_map(&tsa, a_sf, M, a_katoms, 1);
     if (!rc) rc = make_sf_map(&tsb, b_sf, N, b_katoms, 2);
     if (rc) return rc;
+    // output boxes of 128 rows x 128 bytes, 128-byte swizzle (the staging layout of epi_stage)
+    CUtensorMap to;
+    {
+        PFN_encodeTiled enc = get_encode();
+        const int esz = ep.out_bf16 ? 2 : 4;
+        cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+        cuuint64_t strides[1] = {(cuuint64_t)(ep.ldo * esz)};
+        cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 128};
+        cuuint32_t es[2] = {1, 1};
+        if (!enc || enc(&to, ep.out_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                        ep.out, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return 1002;
+    }
     static int sms = 0;
     if (!sms) {
         cudaFuncSetAttribute(k_gemm_mxf4_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2::kBytes);
@@ -605,7 +708,8 @@ static int launch_gemm_2sm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, i
     }
     const int64_t tiles = ((M + 255) / 256) * ((N + 255) / 256);
     const int64_t pairs = tiles < sms / 2 ? tiles : sms / 2;
-    k_gemm_mxf4_2sm<<<(unsigned)(2 * pairs), kThreads, sm2::kBytes, st>>>(ta, tb, tsa, tsb, (int)M, (int)N, (int)K, ep);
+    k_gemm_mxf4_2sm<<<(unsigned)(2 * pairs), kThreads, sm2::kBytes, st>>>(ta, tb, tsa, tsb, to, (int)M, (int)N, (int)K,
+                                                                          ep);
     return (int)cudaGetLastError();
 }
 
@@ -613,7 +717,9 @@ int launch_gemm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, int64_t a_ka
                 const uint8_t* b_sf, int64_t b_katoms, int64_t M, int64_t N, int64_t K, const EpiParams& ep,
                 cudaStream_t st) {
     if (M == 0 || N == 0) return 0;
-    if (g_gemm_2sm && N % 256 == 0 && M >= 256)
+    const int esz = ep.out_bf16 ? 2 : 4;
+    if (g_gemm_2sm && N % 256 == 0 && M >= 256 && (reinterpret_cast<uintptr_t>(ep.out) & 15) == 0 &&
+        (ep.ldo * esz) % 16 == 0)
         return launch_gemm_2sm(a, lda, a_sf, a_katoms, b, ldb, b_sf, b_katoms, M, N, K, ep, st);
     if (N >= 256 && N % 256 == 0)
         return launch_gemm_bn<256>(a, lda, a_sf, a_katoms, b, ldb, b_sf, b_katoms, M, N, K, ep, st);

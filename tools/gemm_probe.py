@@ -18,7 +18,8 @@ for (M, N, K) in [(16384, 4096, 4096), (16384, 4096, 16384)]:
     A = qt.quant_rows(x, 0, _lib.QT_ROUND_RTN)
     B = qt.quant_rows(w, 0, _lib.QT_ROUND_RTN)
     out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
-    for dbg, name in [(0, "baseline (2-CTA pairs)"), (0x40000, "1-CTA 128x256 tiles"), (0x100, "no epilogue math/stores"), (1, "no SF tcgen05.cp after k0"), (3, "no SF loads+cp after k0"),
+    for dbg, name in [(0, "baseline (2-CTA pairs)"), (0x40000, "1-CTA 128x256 tiles"), (0x100, "no epilogue math/stores"),
+                      (0x4000, "grouped-2 walk"), (0x1000, "grouped-4 walk"), (0x2000, "grouped-16 walk"), (1, "no SF tcgen05.cp after k0"), (3, "no SF loads+cp after k0"),
                       (4, "1 MMA per k-tile (1/4 math)"), (8, "no B TMA after k0"), (12, "no B + 1 MMA"),
                       (11, "no B, no SF")]:
         L.qt_debug_set_gemm(dbg)
@@ -34,6 +35,19 @@ for (M, N, K) in [(16384, 4096, 4096), (16384, 4096, 16384)]:
         us = s.elapsed_time(e) * 100
         print(f"M{M} N{N} K{K} {name:32s} {us:8.1f} us  {2 * M * N * K / us / 1e6:7.1f} TF")
     L.qt_debug_set_gemm(0)
+    out32 = torch.empty(M, N, device=dev, dtype=torch.float32)
+    for _ in range(3):
+        qt.gemm(A, B, out=out32)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(10):
+        qt.gemm(A, B, out=out32)
+    e.record()
+    torch.cuda.synchronize()
+    us = s.elapsed_time(e) * 100
+    print(f"M{M} N{N} K{K} {'fp32 output':32s} {us:8.1f} us  {2 * M * N * K / us / 1e6:7.1f} TF")
+    del out32
     # dx-like epilogue (trust mask, FWHT-32, 16/9) at the same shape
     mask = torch.randint(0, 2**31 - 1, (M, N // 32), device=dev, dtype=torch.int32)
     for dbg, name in [(0, "dx epilogue (mask, FWHT, 16/9)"), (0x100, "dx, no epilogue math/stores")]:
