@@ -66,7 +66,10 @@ def test_gemm_structured_scales(qt):
 
 
 @pytest.mark.parametrize("mnk", [(128, 256, 256), (256, 512, 1024), (2048, 1024, 1024), (96, 160, 640),
-                                 (300, 96, 96), (1024, 1152, 2048)])
+                                 (300, 96, 96), (1024, 1152, 2048),
+                                 # 2-CTA pair kernel: M not a multiple of 256 (clipped rows of the second CTA's
+                                 # TMA-stored boxes), K not a multiple of 256 (zero-filled last K tile), one pair
+                                 (288, 512, 640), (640, 768, 1184), (256, 256, 32)])
 def test_gemm_random(qt, oracle, mnk):
     M, N, K = mnk
     r = np.random.default_rng(M + N + K)
@@ -74,6 +77,23 @@ def test_gemm_random(qt, oracle, mnk):
     b = bf16_values(r.standard_t(df=3, size=(N, K)).astype(np.float32))
     e_gpu, e_ref = _check(qt, oracle, a, b)
     print(f"gemm {mnk}: rel err gpu {e_gpu:.3e} ref-fp32 {e_ref:.3e}")
+
+
+@pytest.mark.parametrize("mn", [(288, 512), (1024, 768)])
+def test_gemm_masked_epilogue_fp32_and_bf16_paths_agree(qt, mn):
+    """The staged (TMA-store) epilogue writes the same values in fp32 and bf16 (bf16 = RNE of the fp32)
+    for the masked FWHT . 16/9 epilogue, including clipped edge rows."""
+    M, N = mn
+    K = 512
+    g = torch.Generator(device="cuda").manual_seed(M)
+    from paper_2505_14669_b200 import _lib
+
+    A = qt.quant_rows(torch.randn(M, K, device="cuda", generator=g), _lib.QT_TRANSFORM_NONE, _lib.QT_ROUND_RTN)
+    B = qt.quant_rows(torch.randn(N, K, device="cuda", generator=g), _lib.QT_TRANSFORM_NONE, _lib.QT_ROUND_RTN)
+    mask = torch.randint(-2**31, 2**31 - 1, (M, N // 32), device="cuda", dtype=torch.int32, generator=g)
+    f32 = qt.gemm(A, B, mask=mask, hadamard=True, scale=16 / 9)
+    b16 = qt.gemm(A, B, mask=mask, hadamard=True, scale=16 / 9, out_dtype=torch.bfloat16)
+    assert torch.equal(f32.to(torch.bfloat16), b16)
 
 
 def test_gemm_bf16_out(qt, oracle):
