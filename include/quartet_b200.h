@@ -172,7 +172,8 @@ QT_API int qt_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_sf, const uint8
                  const uint32_t* mask, float scale, void* stream);
 
 /* Experiment hook for the GEMM mainloop studies in tools/gemm_probe.py (0 = production; bit 18 forces the
- * 1-CTA kernel where the 2-CTA pair kernel is the default, for A/B parity tests). */
+ * 1-CTA kernel where the 2-CTA pair kernel is the default, bit 19 runs the pairs in clusters of 8 with TMA
+ * multicast of A and B -- both for A/B parity tests). */
 QT_API void qt_debug_set_gemm(int dbg);
 /* Quantizer path selection for A/B parity tests: mode 0 (production) uses the tensor-core Hadamard
  * quantizer for the backward dual operands, mode 1 forces the CUDA-core path everywhere, mode 2 also

@@ -331,12 +331,12 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 
 template <int CW>
 __device__ __forceinline__ void epi_stage(const uint32_t (&acc)[CW / 32][32], int row, int r_box, int cbase, int M,
-                                          const EpiParams& ep, float2 nz, const CUtensorMap* tmO, uint8_t* box,
+                                          int N, const EpiParams& ep, float2 nz, const CUtensorMap* tmO, uint8_t* box,
                                           int half, bool issuer, int y0) {
-    const bool live = row < M;
 #pragma unroll
     for (int pj = 0; pj < CW / 64; ++pj) {
         const int col0 = cbase + pj * 64;
+        const bool live = row < M && col0 < N;  // tiles past M / N (cluster padding) compute garbage, stores clip
         Pair g;
 #pragma unroll
         for (int i = 0; i < 32; ++i)
@@ -429,15 +429,29 @@ __device__ __forceinline__ void mma_mxf4_2sm(uint32_t d_tmem, uint64_t adesc, ui
 __device__ __forceinline__ void tmem_cp_sf_2sm(uint32_t taddr, uint64_t sdesc) {
     asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc));
 }
-__device__ __forceinline__ void tc_commit_2sm(uint64_t* bar) {
+__device__ __forceinline__ void tc_commit_2sm(uint64_t* bar, uint16_t cta_mask) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
             smem_u32(bar)),
-        "h"((uint16_t)3)
+        "h"(cta_mask)
+        : "memory");
+}
+// 2-SM TMA multicast: the box lands at the same offset in every CTA of cta_mask, each destination's bytes
+// completing on its own pair leader's barrier (mbar_cluster: this pair's leader barrier)
+__device__ __forceinline__ void tma_load_2d_2sm_mc(void* dst, const CUtensorMap* map, uint32_t mbar_cluster, int x, int y,
+                                                   uint16_t cta_mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+        "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(mbar_cluster), "r"(x), "r"(y), "h"(cta_mask)
         : "memory");
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+// NP = CTA pairs per cluster: 1 (cluster of 2) or 4 (cluster of 8: a 2 x 2 block of pair tiles whose A rows
+// are shared along N and B rows along M, each CTA loading half of its A and B boxes and multicasting them to
+// the CTA of the same role in the neighbouring pair, which halves the L2 -> SMEM bytes per FLOP)
+template <int NP>
+__global__ void __launch_bounds__(kThreads, 1)
     k_gemm_mxf4_2sm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmSFA, const __grid_constant__ CUtensorMap tmSFB,
                     const __grid_constant__ CUtensorMap tmO, int M, int N, int K, EpiParams ep) {
@@ -457,10 +471,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = cluster_rank();
-    const bool leader = rank == 0;
+    const uint32_t q = rank & 1, lead_rank = rank & ~1u;    // CTA within its pair, the pair leader's rank
+    const bool leader = q == 0;
+    const int pm = NP == 4 ? (int)((rank >> 1) & 1) : 0, pn = NP == 4 ? (int)(rank >> 2) : 0;
+    const uint16_t pair_mask = (uint16_t)(3u << lead_rank), all_mask = (uint16_t)((1u << (2 * NP)) - 1);
     const int nk = (K + 255) / 256;
-    const int tiles_n = (N + BN - 1) / BN, tiles = ((M + 255) / 256) * tiles_n;
-    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const int tiles_m = (M + 255) / 256, tiles_n = (N + BN - 1) / BN;
+    const int sup_m = NP == 4 ? (tiles_m + 1) / 2 : tiles_m, sup_n = NP == 4 ? (tiles_n + 1) / 2 : tiles_n;
+    const int tiles = sup_m * sup_n;                        // (super-)tiles walked by the cluster
+    const int cid = blockIdx.x / (2 * NP), ncl = gridDim.x / (2 * NP);
     // tile walk: grouped (gm row blocks per column sweep) for long K, row-major otherwise; dbg 0x1000 / 0x2000
     // force grouped-4 / grouped-16 (timing experiments)
     const int gm = (ep.dbg & 0x1000) ? 4 : (ep.dbg & 0x2000) ? 16 : (ep.dbg & 0x4000) ? 2 : (K >= 8192 ? 8 : 0);
@@ -472,7 +491,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tma_prefetch(&tmSFB);
         for (int s = 0; s < sm2::kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], NP);  // one commit per pair whose smem this CTA's loads fill
         }
         mbar_init(tmem_full, 1);
         mbar_init(tmem_empty, 2 * kEpiWarps);
@@ -493,17 +512,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         // producer (warp-uniform loop, elected issue): this CTA's A half and B half, its A scale atoms and all
         // 256 B rows' atoms, completing on the leader's full barrier
         uint32_t s = 0, ph = 0;
+        const uint16_t mask_a = NP == 4 ? (uint16_t)((1u << ((pm << 1) | q)) | (1u << (4 | (pm << 1) | q))) : 0;
+        const uint16_t mask_b = NP == 4 ? (uint16_t)((1u << ((pn << 2) | q)) | (1u << ((pn << 2) | 2 | q))) : 0;
         for (int tile = cid; tile < tiles; tile += ncl) {
             int mb, nb;
-            tile_mn(tile, (M + 255) / 256, tiles_n, mb, nb, gm);
-            const int m0 = mb * 256 + 128 * rank, n0 = nb * BN;
+            tile_mn(tile, sup_m, sup_n, mb, nb, gm);
+            if (NP == 4) {
+                mb = 2 * mb + pm;
+                nb = 2 * nb + pn;
+            }
+            const int m0 = mb * 256 + 128 * (int)q, n0 = nb * BN;
             for (int kt = 0; kt < nk; ++kt) {
                 mbar_wait(&empty[s], ph ^ 1);
                 if (elect_one()) {
-                    const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+                    const uint32_t fb = mapa_shared(smem_u32(&full[s]), lead_rank);
                     if (leader) mbar_arrive_expect_tx(&full[s], 2 * sm2::kStage);
-                    tma_load_2d_2sm(sA + s * sm2::kA, &tmA, fb, kt * kBKBytes, m0);
-                    tma_load_2d_2sm(sB + s * sm2::kB, &tmB, fb, kt * kBKBytes, n0 + 128 * (int)rank);
+                    if (NP == 4) {
+                        // my half of the A box (rows + 64 pn) to both pairs on this M block, my half of the B box
+                        // (rows + 64 pm) to both pairs on this N block
+                        tma_load_2d_2sm_mc(sA + s * sm2::kA + pn * 8192, &tmA, fb, kt * kBKBytes, m0 + 64 * pn, mask_a);
+                        tma_load_2d_2sm_mc(sB + s * sm2::kB + pm * 8192, &tmB, fb, kt * kBKBytes,
+                                           n0 + 128 * (int)q + 64 * pm, mask_b);
+                    } else {
+                        tma_load_2d_2sm(sA + s * sm2::kA, &tmA, fb, kt * kBKBytes, m0);
+                        tma_load_2d_2sm(sB + s * sm2::kB, &tmB, fb, kt * kBKBytes, n0 + 128 * (int)q);
+                    }
                     // scale atoms (u32 view, 1 KB = 256 words per K tile): A rows of this CTA, all 256 B rows
                     tma_load_2d_2sm(sSFA + s * sm2::kSFA, &tmSFA, fb, kt * 256, m0 / 128);
                     tma_load_2d_2sm(sSFB + s * sm2::kSFB, &tmSFB, fb, kt * 256, n0 / 128);
@@ -554,7 +587,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         for (int j = 0; j < 4; ++j)
                             mma_mxf4_2sm(t_acc, ad + 2 * j, bd + 2 * j, (j & 1) ? id2 : id0, t_sfa + so + (j >> 1) * 4,
                                          t_sfb + so + (j >> 1) * 8, (kt | j) != 0 ? 1u : 0u);
-                        tc_commit_2sm(&empty[s]);
+                        tc_commit_2sm(&empty[s], all_mask);
                         s = s + 1 == sm2::kStages ? 0u : s + 1;
                         ph ^= s == 0 ? 1u : 0u;
                         if (it + 1 < total) {
@@ -563,7 +596,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             sf_copy(s, (uint32_t)((it + 1) & 3));
                         }
                     }
-                    tc_commit_2sm(tmem_full);
+                    tc_commit_2sm(tmem_full, pair_mask);
                 }
             }
             __syncwarp();
@@ -572,13 +605,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int quad = warp % 4, half = (warp - 2) / 4;
         const bool issuer = ((warp - 2) & 3) == 0 && lane == 0;  // one thread per column half issues the stores
         const float2 nz = opaque_nz2();
-        const uint32_t te_leader = mapa_shared(smem_u32(tmem_empty), 0);
+        const uint32_t te_leader = mapa_shared(smem_u32(tmem_empty), lead_rank);
         uint8_t* box = sBox + half * sm2::kBox;
         int tcount = 0;
         for (int tile = cid; tile < tiles; tile += ncl, ++tcount) {
             int mb, nb;
-            tile_mn(tile, (M + 255) / 256, tiles_n, mb, nb, gm);
-            const int m0 = mb * 256 + 128 * rank, n0 = nb * BN;
+            tile_mn(tile, sup_m, sup_n, mb, nb, gm);
+            if (NP == 4) {
+                mb = 2 * mb + pm;
+                nb = 2 * nb + pn;
+            }
+            const int m0 = mb * 256 + 128 * (int)q, n0 = nb * BN;
             const int row = m0 + quad * 32 + lane, cbase = n0 + half * CW;
             mbar_wait(tmem_full, tcount & 1);
             tc_fence_after();
@@ -591,7 +628,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(te_leader);  // the leader may start the next tile
             if (ep.dbg & 0x100) continue;                   // timing only: no epilogue math/stores
-            epi_stage<CW>(acc, row, quad * 32 + lane, cbase, M, ep, nz, &tmO, box, half, issuer, m0);
+            epi_stage<CW>(acc, row, quad * 32 + lane, cbase, M, N, ep, nz, &tmO, box, half, issuer, m0);
         }
         if (issuer) bulk_wait0();
     }
@@ -676,12 +713,64 @@ static int make_sf_map(CUtensorMap* m, const uint8_t* sf, int64_t rows, int64_t 
     return r == CUDA_SUCCESS ? 0 : 1002;
 }
 
+int g_gemm_cluster8 = 0;  // 1: clusters of 4 pairs with TMA multicast (measured slower: fewer co-resident SMs)
+
+template <int NP>
+static int launch_2sm_np(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tsa, const CUtensorMap& tsb,
+                         const CUtensorMap& to, int64_t M, int64_t N, int64_t K, const EpiParams& ep, cudaStream_t st) {
+    static int max_clusters = 0;
+    if (!max_clusters) {
+        cudaFuncSetAttribute(k_gemm_mxf4_2sm<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2::kBytes);
+        if (NP == 4) cudaFuncSetAttribute(k_gemm_mxf4_2sm<NP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2 * NP;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(2 * NP * 64, 1, 1);
+        cfg.blockDim = dim3(kThreads, 1, 1);
+        cfg.dynamicSmemBytes = sm2::kBytes;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_gemm_mxf4_2sm<NP>, &cfg) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            int dev = 0, sms = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            n = sms / (2 * NP);
+        }
+        max_clusters = n;
+    }
+    const int64_t tm = (M + 255) / 256, tn = (N + 255) / 256;
+    const int64_t tiles = NP == 4 ? ((tm + 1) / 2) * ((tn + 1) / 2) : tm * tn;
+    const int64_t clusters = tiles < max_clusters ? tiles : max_clusters;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2 * NP;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(2 * NP * clusters), 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = sm2::kBytes;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemm_mxf4_2sm<NP>, ta, tb, tsa, tsb, to, (int)M, (int)N, (int)K, ep);
+    return (int)e;
+}
+
 static int launch_gemm_2sm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, int64_t a_katoms, const uint8_t* b,
                            int64_t ldb, const uint8_t* b_sf, int64_t b_katoms, int64_t M, int64_t N, int64_t K,
                            const EpiParams& ep, cudaStream_t st) {
+    // cluster of 4 pairs (multicast) when there is at least a 2 x 2 block of pair tiles
+    const bool c8 = g_gemm_cluster8 && M >= 512 && N >= 512;
+    const int box_rows = c8 ? 64 : 128;
     CUtensorMap ta, tb, tsa, tsb;
-    int rc = make_codes_map(&ta, a, M, K / 2, lda, 128);
-    if (!rc) rc = make_codes_map(&tb, b, N, K / 2, ldb, 128);
+    int rc = make_codes_map(&ta, a, M, K / 2, lda, box_rows);
+    if (!rc) rc = make_codes_map(&tb, b, N, K / 2, ldb, box_rows);
     if (!rc) rc = make_sf_map(&tsa, a_sf, M, a_katoms, 1);
     if (!rc) rc = make_sf_map(&tsb, b_sf, N, b_katoms, 2);
     if (rc) return rc;
@@ -699,18 +788,8 @@ static int launch_gemm_2sm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, i
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return 1002;
     }
-    static int sms = 0;
-    if (!sms) {
-        cudaFuncSetAttribute(k_gemm_mxf4_2sm, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2::kBytes);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const int64_t tiles = ((M + 255) / 256) * ((N + 255) / 256);
-    const int64_t pairs = tiles < sms / 2 ? tiles : sms / 2;
-    k_gemm_mxf4_2sm<<<(unsigned)(2 * pairs), kThreads, sm2::kBytes, st>>>(ta, tb, tsa, tsb, to, (int)M, (int)N, (int)K,
-                                                                          ep);
-    return (int)cudaGetLastError();
+    return c8 ? launch_2sm_np<4>(ta, tb, tsa, tsb, to, M, N, K, ep, st)
+              : launch_2sm_np<1>(ta, tb, tsa, tsb, to, M, N, K, ep, st);
 }
 
 int launch_gemm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, int64_t a_katoms, const uint8_t* b, int64_t ldb,

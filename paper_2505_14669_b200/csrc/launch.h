@@ -66,6 +66,7 @@ int launch_tcq_dual(const void* x, int64_t ldx, int64_t R, int64_t C, const uint
                     const uint32_t* col_sign_bits, float prescale, const QuantOut& row_out, const QuantOut& col_out,
                     int* fallbacks, cudaStream_t st);
 extern int g_gemm_2sm;
+extern int g_gemm_cluster8;
 int launch_gemm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, int64_t a_katoms, const uint8_t* b, int64_t ldb,
                 const uint8_t* b_sf, int64_t b_katoms, int64_t M, int64_t N, int64_t K, const EpiParams& ep,
                 cudaStream_t st);

@@ -49,7 +49,7 @@ struct TqArgs {
     QuantOut row_out, col_out;   // G [R, C], G_t [C, R]
     float prescale;
     int* fallbacks;              // nullable: groups recomputed exactly
-    int dbg;                     // experiment knobs (0 in production): 1 skip quantize, 2 skip B build, 4 skip TMEM ld
+    int dbg;                     // experiment knobs (0 in production): 1 skip quantize, 2 skip B build, 4 skip TMEM ld, 8 skip stores
 };
 
 // Four of the 1024 16-byte chunks of a tile's 8 signed Hadamard blocks (4 row-pass blocks from the column
@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(kTqThreads, 1)
                     // (r % 32) * 16 + ((r / 32) % 4) * 4 + g
                     uint8_t* sp = out.sf + ((orow >> 7) * out.katoms + (kb >> 7)) * 512 + (orow & 31) * 16 +
                                   ((orow >> 5) & 3) * 4 + g0;
+                    if ((a.dbg & 8) && orow != -12345) continue;  // timing only: no output stores
                     if (kb + 32 * g0 + 32 < lim_k) {
                         *reinterpret_cast<uint4*>(cp) = c0d;
                         *reinterpret_cast<uint4*>(cp + 16) = c1d;

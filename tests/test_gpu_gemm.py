@@ -135,3 +135,17 @@ def test_gemm_1cta_kernel(qt, oracle, mnk):
         test_gemm_random(qt, oracle, mnk)
     finally:
         L.qt_debug_set_gemm(0)
+
+
+@pytest.mark.parametrize("mnk", [(2048, 1024, 1024), (1024, 1152, 2048), (640, 768, 1184)])
+def test_gemm_cluster8_multicast_kernel(qt, oracle, mnk):
+    """The opt-in cluster-of-8 variant (2 x 2 pair tiles, A and B boxes multicast between pairs, partial
+    super-tiles at the edges) matches the oracle like the default path."""
+    from paper_2505_14669_b200 import _lib
+
+    L = _lib.load()
+    L.qt_debug_set_gemm(0x80000)
+    try:
+        test_gemm_random(qt, oracle, mnk)
+    finally:
+        L.qt_debug_set_gemm(0)

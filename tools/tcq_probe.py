@@ -9,7 +9,7 @@ L = qt.load()
 x = torch.randn(16384, 4096, device="cuda").to(torch.bfloat16)
 rs, cs = sign_bits(5, x.shape[1], "cuda"), sign_bits(9, x.shape[0], "cuda")
 f = lambda: quant_dual(x, _lib.QT_ROUND_RTN, transform=_lib.QT_TRANSFORM_RANDOMIZED, signs=rs, col_signs=cs, prescale=0.75)
-for dbg, name in ((0, "full"), (1, "skip quantize"), (2, "skip B build"), (3, "skip both"), (4, "skip TMEM ld"), (5, "skip ld+quant"), (7, "skip all")):
+for dbg, name in ((0, "full"), (1, "skip quantize"), (2, "skip B build"), (3, "skip both"), (4, "skip TMEM ld"), (5, "skip ld+quant"), (7, "skip all"), (8, "skip stores")):
     L.qt_debug_set_quant(dbg << 4, None)
     f(); torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
