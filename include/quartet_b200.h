@@ -183,6 +183,15 @@ QT_API void qt_debug_set_gemm(int dbg);
  * 3 for mode 3) counts groups a tensor-core path re-decided exactly.  Not thread-safe; tests only. */
 QT_API void qt_debug_set_quant(int mode, int* fallbacks);
 
+/* ---- Llama-loop glue (not on the Quartet path; llama.py): fused bf16 elementwise kernels, fp32 math.
+ * qt_rope: half-split rotary embedding of x [rows, heads, head_dim] (row r at position r % seq) with
+ *   cos/sin tables [seq, head_dim]; backward != 0 applies the transposed rotation (dx from dy).
+ * qt_swiglu: forward out0 = silu(gate) * up; backward (dy given) out0 = d gate, out1 = d up.  n % 8 == 0. */
+QT_API int qt_rope(const void* x, void* out, int64_t rows, int heads, int head_dim, int seq, const void* cos,
+                   const void* sin, int backward, void* stream);
+QT_API int qt_swiglu(const void* gate, const void* up, const void* dy, void* out0, void* out1, int64_t n,
+                     int backward, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,6 +24,8 @@ from dataclasses import dataclass
 import torch
 import torch.nn.functional as F
 
+from . import _lib
+from .mxfp4 import _stream
 from .nn import QuartetLinear
 
 GROUP = 32
@@ -82,11 +84,62 @@ def _rope(seq: int, dh: int, base: float, device):
     return torch.cos(f).to(torch.bfloat16), torch.sin(f).to(torch.bfloat16)
 
 
-def _apply_rope(x, cos, sin):  # x [B, H, S, dh] bf16
+def _apply_rope_torch(x, cos, sin):  # x [B, H, S, dh] bf16 (reference formulation, tests)
     h = x.shape[-1] // 2
     rot = torch.cat((-x[..., h:], x[..., :h]), dim=-1)
     S = x.shape[2]
     return x * cos[:S] + rot * sin[:S]
+
+
+def _rope_call(x, cos, sin, backward: bool):
+    """x [B, S, H, dh] contiguous bf16 -> rotated copy (csrc/glue.cu, one pass)."""
+    B, S, H, dh = x.shape
+    out = torch.empty_like(x)
+    _lib.check(_lib.load().qt_rope(x.data_ptr(), out.data_ptr(), B * S, H, dh, S, cos.data_ptr(), sin.data_ptr(),
+                                   int(backward), _stream(x.device)), "qt_rope")
+    return out
+
+
+class _Rope(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, cos, sin):
+        ctx.save_for_backward(cos, sin)
+        return _rope_call(x.contiguous(), cos, sin, False)
+
+    @staticmethod
+    def backward(ctx, dy):
+        cos, sin = ctx.saved_tensors
+        return _rope_call(dy.contiguous(), cos, sin, True), None, None
+
+
+class _SwiGLU(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, g, u):
+        g, u = g.contiguous(), u.contiguous()
+        ctx.save_for_backward(g, u)
+        out = torch.empty_like(g)
+        _lib.check(_lib.load().qt_swiglu(g.data_ptr(), u.data_ptr(), None, out.data_ptr(), None, g.numel(), 0,
+                                         _stream(g.device)), "qt_swiglu")
+        return out
+
+    @staticmethod
+    def backward(ctx, dy):
+        g, u = ctx.saved_tensors
+        dy = dy.contiguous()
+        dg, du = torch.empty_like(g), torch.empty_like(u)
+        _lib.check(_lib.load().qt_swiglu(g.data_ptr(), u.data_ptr(), dy.data_ptr(), dg.data_ptr(), du.data_ptr(),
+                                         g.numel(), 1, _stream(g.device)), "qt_swiglu")
+        return dg, du
+
+
+def swiglu(g, u):
+    """silu(g) * u, fused forward and backward (bf16)."""
+    return _SwiGLU.apply(g, u)
+
+
+def rope(x, cos, sin):
+    """Rotary embedding of x [B, S, H, dh] bf16 (half-split layout), fused forward and backward."""
+    return _Rope.apply(x, cos[: x.shape[1]], sin[: x.shape[1]])
 
 
 class Block(torch.nn.Module):
@@ -107,14 +160,13 @@ class Block(torch.nn.Module):
         B, S, d = x.shape
         H, dh = self.n_head, d // self.n_head
         a = self.attn_norm(x)
-        q = self.q(a).view(B, S, H, dh).transpose(1, 2)
-        k = self.k(a).view(B, S, H, dh).transpose(1, 2)
+        q = rope(self.q(a).view(B, S, H, dh), cos, sin).transpose(1, 2)
+        k = rope(self.k(a).view(B, S, H, dh), cos, sin).transpose(1, 2)
         v = self.v(a).view(B, S, H, dh).transpose(1, 2)
-        q, k = _apply_rope(q, cos, sin), _apply_rope(k, cos, sin)
         att = F.scaled_dot_product_attention(q, k, v, is_causal=True)
         x = x + self.o(att.transpose(1, 2).reshape(B, S, d))
         m = self.mlp_norm(x)
-        return x + self.down(F.silu(self.gate(m)) * self.up(m))
+        return x + self.down(swiglu(self.gate(m), self.up(m)))
 
 
 class LlamaQuartet(torch.nn.Module):

@@ -53,3 +53,39 @@ def test_lr_schedule_matches_reference(llama):
     assert llama.lr_at(0, steps, lr) == pytest.approx(0.1)
     assert llama.lr_at(9, steps, lr) == pytest.approx(1.0)
     assert llama.lr_at(99, steps, lr) == pytest.approx(0.0, abs=1e-12)
+
+
+def test_fused_rope_matches_fp32_reference(llama):
+    """csrc/glue.cu rotary embedding vs a plain fp32 torch reference (forward and the transposed backward);
+    tolerance: one bf16 rounding of the fp32 result (2^-8 relative, plus tiny absolute)."""
+    B, S, H, dh = 2, 64, 4, 128
+    cos, sin = llama._rope(S, dh, 10000.0, "cuda")
+    x = torch.randn(B, S, H, dh, device="cuda").to(torch.bfloat16).requires_grad_(True)
+    y = llama.rope(x, cos, sin)
+    xf = x.detach().float().transpose(1, 2)          # [B, H, S, dh]
+    h = dh // 2
+    rot = torch.cat((-xf[..., h:], xf[..., :h]), dim=-1)
+    ref = (xf * cos.float() + rot * sin.float()).transpose(1, 2)
+    torch.testing.assert_close(y.float(), ref, rtol=2 ** -8, atol=1e-6)
+    dy = torch.randn_like(y)
+    (gx,) = torch.autograd.grad(y, x, dy)
+    xr = x.detach().float().requires_grad_(True)
+    xrt = xr.transpose(1, 2)
+    rr = torch.cat((-xrt[..., h:], xrt[..., :h]), dim=-1)
+    yr = (xrt * cos.float() + rr * sin.float()).transpose(1, 2)
+    (gr,) = torch.autograd.grad(yr, xr, dy.float())
+    torch.testing.assert_close(gx.float(), gr, rtol=2 ** -8, atol=1e-6)
+
+
+def test_fused_swiglu_matches_fp32_reference(llama):
+    g = torch.randn(512, 384, device="cuda").to(torch.bfloat16).requires_grad_(True)
+    u = torch.randn(512, 384, device="cuda").to(torch.bfloat16).requires_grad_(True)
+    y = llama.swiglu(g, u)
+    gf, uf = g.detach().float().requires_grad_(True), u.detach().float().requires_grad_(True)
+    yf = torch.nn.functional.silu(gf) * uf
+    torch.testing.assert_close(y.float(), yf, rtol=2 ** -7, atol=1e-5)
+    dy = torch.randn_like(y)
+    dg, du = torch.autograd.grad(y, (g, u), dy)
+    dgf, duf = torch.autograd.grad(yf, (gf, uf), dy.float())
+    torch.testing.assert_close(dg.float(), dgf, rtol=2 ** -7, atol=1e-4)
+    torch.testing.assert_close(du.float(), duf, rtol=2 ** -7, atol=1e-4)
