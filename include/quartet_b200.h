@@ -176,10 +176,9 @@ QT_API int qt_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_sf, const uint8
  * multicast of A and B -- both for A/B parity tests). */
 QT_API void qt_debug_set_gemm(int dbg);
 /* Quantizer path selection for A/B parity tests: mode 0 (production) uses the tensor-core Hadamard
- * quantizer for the backward dual operands, mode 1 forces the CUDA-core path everywhere, mode 2 also
- * routes qt_quant_fused to the (slower, experimental) tensor-core transposed requantization, mode 3 routes
+ * quantizer for the backward dual operands, mode 1 forces the CUDA-core path everywhere, mode 3 routes
  * the bf16 QuEST forward of qt_quant_fused to the all-tensor-core kernel (checked QuEST + checked RTN,
- * experimental, about par with the CUDA-core kernel); `fallbacks` (nullable device ints: 1 for modes 0/2,
+ * experimental, about par with the CUDA-core kernel); `fallbacks` (nullable device ints: 1 for mode 0,
  * 3 for mode 3) counts groups a tensor-core path re-decided exactly.  Not thread-safe; tests only. */
 QT_API void qt_debug_set_quant(int mode, int* fallbacks);
 

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(BUILD, "libquartet_b200.so")
-SOURCES = ["quant.cu", "tcq.cu", "tcq_fwd.cu", "tcq_x.cu", "gemm.cu", "glue.cu", "capi.cu"]
+SOURCES = ["quant.cu", "tcq.cu", "tcq_x.cu", "gemm.cu", "glue.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr"]

@@ -10,7 +10,7 @@ static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) 
 static inline uint64_t sr_base_of(uint64_t seed) { return mix64(seed ^ mix64(kDomainSR)); }
 
 static int g_gemm_dbg = 0;  // experiment knobs for qt_debug_set_gemm (never set in production)
-static int g_quant_mode = 0;  // qt_debug_set_quant: 0 production, 1 CUDA cores only, 2 tensor-core fused forward
+static int g_quant_mode = 0;  // qt_debug_set_quant: 0 production, 1 CUDA cores only, 3 tensor-core QuEST forward
 static int* g_quant_fallbacks = nullptr;
 
 extern "C" {
@@ -168,14 +168,6 @@ int qt_quant_fused(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64
         int rc3 = launch_tcq_xq(x, ldx, rows, cols, ro, col_sign_bits, col_prescale, co, g_quant_fallbacks,
                                 (cudaStream_t)stream);
         return rc3 == 1001 || rc3 == 1002 ? QT_ERR_TMA : rc3;
-    }
-    if (g_quant_mode == 2 && col_rounding == QT_ROUND_RTN && col_transform == QT_TRANSFORM_RANDOMIZED &&
-        row_transform != QT_TRANSFORM_RANDOMIZED) {
-        // X_t / W_t on the tensor cores (checked RTN, exact per-group fallback): bit-identical, but measured
-        // slower than the CUDA-core fused kernel (the QuEST row pass loses occupancy), so opt-in only
-        int rc2 = launch_tcq_fwd(x, in_dtype, ldx, rows, cols, rc, ro, col_sign_bits, col_prescale, co,
-                                 g_quant_fallbacks, (cudaStream_t)stream);
-        return rc2 == 1001 || rc2 == 1002 ? QT_ERR_TMA : rc2;
     }
     MxIn mx{nullptr, 0, nullptr, 0};
     return launch_quant_tile(x, in_dtype, ldx, mx, rows, cols, &rc, &ro, &cc, &co, 1, (cudaStream_t)stream);

@@ -55,9 +55,6 @@ int launch_quant_rows(const void* x, int in_type, int64_t ldx, int64_t rows, int
 int launch_quant_tile(const void* x, int in_type, int64_t ldx, const MxIn& mx, int64_t R, int64_t C,
                       const QuantCfg* row_cfg, const QuantOut* row_out, const QuantCfg* col_cfg,
                       const QuantOut* col_out, int col_from_codes, cudaStream_t st);
-int launch_tcq_fwd(const void* x, int in_type, int64_t ldx, int64_t R, int64_t C, const QuantCfg& rc,
-                   const QuantOut& row_out, const uint32_t* col_sign_bits, float col_prescale, const QuantOut& col_out,
-                   int* fallbacks, cudaStream_t st);
 int launch_tcq_xq(const void* x, int64_t ldx, int64_t R, int64_t C, const QuantOut& row_out,
                   const uint32_t* col_sign_bits, float col_prescale, const QuantOut& col_out, int* fallbacks,
                   cudaStream_t st);

@@ -1,5 +1,5 @@
 // tcq.cuh -- shared pieces of the tensor-core Hadamard quantizers (tcq.cu: backward dy operands,
-// tcq_fwd.cu: forward operand + transposed requantization).  See tcq.cu for the error-bound proof.
+// tcq_x.cu: forward activation operand + transposed requantization).  See tcq.cu for the error-bound proof.
 #pragma once
 #include "launch.h"
 #include "qgroup.cuh"
