@@ -71,8 +71,35 @@ class RMSNorm(torch.nn.Module):
         self.weight = torch.nn.Parameter(torch.ones(d, device=device))
         self.eps = eps
 
-    def forward(self, x):  # fused torch kernel in bf16 (fp32 statistics)
-        return F.rms_norm(x.to(torch.bfloat16), (x.shape[-1],), self.weight.to(torch.bfloat16), self.eps)
+    def forward(self, x):  # bf16 in / out, fp32 statistics and weight
+        d = x.shape[-1]
+        if d % 256 == 0 and d <= 2048:  # csrc/glue.cu, one pass each way
+            return _RMSNormFn.apply(x.to(torch.bfloat16), self.weight, self.eps)
+        return F.rms_norm(x.to(torch.bfloat16), (d,), self.weight.to(torch.bfloat16), self.eps)
+
+
+class _RMSNormFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, w, eps):
+        x2 = x.contiguous().view(-1, x.shape[-1])
+        out = torch.empty_like(x2)
+        rstd = torch.empty(x2.shape[0], dtype=torch.float32, device=x.device)
+        _lib.check(_lib.load().qt_rmsnorm(x2.data_ptr(), w.data_ptr(), None, out.data_ptr(), rstd.data_ptr(), None,
+                                          x2.shape[0], x2.shape[1], float(eps), 0, _stream(x.device)), "qt_rmsnorm")
+        ctx.save_for_backward(x2, w, rstd)
+        ctx.eps = eps
+        return out.view(x.shape)
+
+    @staticmethod
+    def backward(ctx, dy):
+        x2, w, rstd = ctx.saved_tensors
+        dy2 = dy.contiguous().view(x2.shape)
+        dx = torch.empty_like(x2)
+        dw = torch.zeros(x2.shape[1], dtype=torch.float32, device=x2.device)
+        _lib.check(_lib.load().qt_rmsnorm(x2.data_ptr(), w.data_ptr(), dy2.data_ptr(), dx.data_ptr(), rstd.data_ptr(),
+                                          dw.data_ptr(), x2.shape[0], x2.shape[1], float(ctx.eps), 1,
+                                          _stream(x2.device)), "qt_rmsnorm")
+        return dx.view(dy.shape), dw.to(w.dtype), None
 
 
 def _rope(seq: int, dh: int, base: float, device):

@@ -89,3 +89,22 @@ def test_fused_swiglu_matches_fp32_reference(llama):
     dgf, duf = torch.autograd.grad(yf, (gf, uf), dy.float())
     torch.testing.assert_close(dg.float(), dgf, rtol=2 ** -7, atol=1e-4)
     torch.testing.assert_close(du.float(), duf, rtol=2 ** -7, atol=1e-4)
+
+
+def test_fused_rmsnorm_matches_fp32_reference(llama):
+    """csrc/glue.cu RMSNorm (forward, dx, dw) vs an fp32 torch reference; tolerance: bf16 rounding of the
+    outputs (2^-7 relative) and fp32 summation order for dw."""
+    x = torch.randn(1000, 1280, device="cuda").to(torch.bfloat16).requires_grad_(True)
+    norm = llama.RMSNorm(1280, device="cuda")
+    with torch.no_grad():
+        norm.weight.uniform_(0.5, 1.5)
+    y = norm(x)
+    xf = x.detach().float().requires_grad_(True)
+    wf = norm.weight.detach().clone().requires_grad_(True)
+    yf = xf * torch.rsqrt((xf * xf).mean(-1, keepdim=True) + norm.eps) * wf
+    torch.testing.assert_close(y.float(), yf, rtol=2 ** -7, atol=1e-5)
+    dy = torch.randn_like(y)
+    dx, dw = torch.autograd.grad(y, (x, norm.weight), dy)
+    dxf, dwf = torch.autograd.grad(yf, (xf, wf), dy.float())
+    torch.testing.assert_close(dx.float(), dxf, rtol=2 ** -7, atol=1e-4)
+    torch.testing.assert_close(dw, dwf, rtol=1e-4, atol=1e-3)
