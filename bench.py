@@ -349,7 +349,7 @@ def run_ours(args, rank, world, local_rank):
         "bf16_cublas": {"value": round(flops_per_step(T) / (bf16_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
                         "ms_per_step": round(bf16_ms, 4), "speedup_ours": round(bf16_ms / ms, 3),
                         "what": "torch.matmul bf16: y = x W^T, dx = dy W, dw = dy^T x per shape"},
-        "roofline": {"kernel": "k_gemm_mxf4 (tcgen05.mma kind::mxf4)", "bound": "tensor",
+        "roofline": {"kernel": "k_gemm_mxf4_2sm (tcgen05.mma.cta_group::2.kind::mxf4, 2-CTA pairs; 1-CTA k_gemm_mxf4 for other shapes)", "bound": "tensor",
                      "achieved": round(gemm_tflops, 1), "peak": round(fp4_peak, 1), "unit": "TFLOP/s",
                      "frac": round(gemm_tflops / fp4_peak, 4), "traffic": traffic,
                      "peak_source": f"4 x bf16_tflops of {peaks['source']} (dense FP4 = 4x dense BF16 on B200); "
