@@ -262,6 +262,77 @@ class GradBucket:
             off += n
 
 
+class OverlappedGradBuckets:
+    """Bucketed data-parallel gradient exchange overlapped with backward: parameters are grouped,
+    in reverse registration order (roughly the order backward produces their gradients), into buckets of
+    about `bucket_mb`; a post-accumulate-grad hook launches a bucket's bf16 all-reduce (async) as soon as its
+    last gradient is ready, while backward keeps running on the remaining layers.  finish() waits, divides by
+    the world size and copies the means back into .grad.  Same values as GradBucket (bf16 on the wire, one
+    SUM per element)."""
+
+    def __init__(self, params, bucket_mb: float = 25.0, comm_dtype=torch.bfloat16, group=None):
+        self.params = [p for p in params if p.requires_grad]
+        self.group, self.comm_dtype = group, comm_dtype
+        self.buckets, cur, size = [], [], 0
+        limit = int(bucket_mb * 2**20)
+        for p in reversed(self.params):
+            cur.append(p)
+            size += p.numel() * torch.finfo(comm_dtype).bits // 8
+            if size >= limit:
+                self.buckets.append(cur)
+                cur, size = [], 0
+        if cur:
+            self.buckets.append(cur)
+        self.bucket_of = {}
+        for i, b in enumerate(self.buckets):
+            for p in b:
+                self.bucket_of[p] = i
+        self.bufs = [torch.empty(sum(p.numel() for p in b), dtype=comm_dtype, device=b[0].device)
+                     for b in self.buckets]
+        self._pending = [len(b) for b in self.buckets]
+        self._work = [None] * len(self.buckets)
+        self._hooks = [p.register_post_accumulate_grad_hook(self._ready) for p in self.params]
+
+    def _active(self) -> bool:
+        import torch.distributed as dist
+
+        return dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1
+
+    def _ready(self, p) -> None:
+        if not self._active():
+            return
+        i = self.bucket_of[p]
+        self._pending[i] -= 1
+        if self._pending[i] == 0:
+            import torch.distributed as dist
+
+            off = 0
+            for q in self.buckets[i]:
+                n = q.numel()
+                self.bufs[i][off:off + n].copy_(q.grad.reshape(-1))
+                off += n
+            self._work[i] = dist.all_reduce(self.bufs[i], group=self.group, async_op=True)
+
+    def finish(self) -> None:
+        if not self._active():
+            return
+        import torch.distributed as dist
+
+        world = dist.get_world_size(self.group)
+        for i, b in enumerate(self.buckets):
+            if self._work[i] is None:  # a bucket whose grads were not all produced this step
+                raise RuntimeError(f"gradient bucket {i} was not reduced (unused parameters?)")
+            self._work[i].wait()
+            self.bufs[i].div_(world)
+            off = 0
+            for q in b:
+                n = q.numel()
+                q.grad.copy_(self.bufs[i][off:off + n].view_as(q.grad))
+                off += n
+            self._work[i] = None
+            self._pending[i] = len(b)
+
+
 class Trainer:
     """AdamW / clip / schedule of the reference loop (train.py:325-382) around LlamaQuartet, data parallel."""
 
@@ -271,7 +342,7 @@ class Trainer:
         params = [p for p in model.parameters() if p.requires_grad]
         self.opt = torch.optim.AdamW(params, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay,
                                      fused=params[0].is_cuda)
-        self.bucket = GradBucket(params)
+        self.bucket = OverlappedGradBuckets(params)
         self.step_i = 0
 
     def step(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
@@ -281,8 +352,8 @@ class Trainer:
         logits = self.model(tokens)
         loss = F.cross_entropy(logits.view(-1, logits.shape[-1]), targets.reshape(-1))
         self.opt.zero_grad(set_to_none=False)
-        loss.backward()
-        self.bucket.allreduce()
+        loss.backward()                # bucket all-reduces start inside backward (hooks)
+        self.bucket.finish()
         torch.nn.utils.clip_grad_norm_(self.bucket.params, self.grad_clip)
         self.opt.step()
         self.step_i += 1
