@@ -205,6 +205,7 @@ def run_ours(args, rank, world, local_rank):
         data.append((x, w, dy))
 
     def step(xi):
+        pending = []
         for i, (x, w, dy) in enumerate(data):
             # the step's backward seed is known at forward time (train.py:346-348), so X_t / W_t come
             # out of the forward read of X / W (qt_quant_fused)
@@ -214,10 +215,13 @@ def run_ours(args, rank, world, local_rank):
                                 token_offset=rank * T, total_tokens=world * T)
             dx, dw = qt.backward(dy, ctx, xi=xi * 3 + i, dx_dtype=torch.bfloat16, dw_dtype=torch.float32,
                                  check_finite=False, token_offset=rank * T, total_tokens=world * T)
-            if world > 1:  # data parallel: the token-sum of dW is the only exchange (bf16, NCCL)
+            if world > 1:  # data parallel: the token-sum of dW is the only exchange (bf16, NCCL); it runs
+                # asynchronously on NCCL's stream while the next shape computes, and is waited for at step end
                 buf = dw.to(torch.bfloat16)
-                dist.all_reduce(buf)
-                dw.copy_(buf)
+                pending.append((dist.all_reduce(buf, async_op=True), buf, dw))
+        for work, buf, dw in pending:
+            work.wait()
+            dw.copy_(buf)
 
     for i in range(args.warmup):
         step(i)
@@ -457,6 +461,10 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    # test hook: QT_BENCH_ONE_GPU=1 puts every rank on cuda:0 (with QT_BENCH_BACKEND=gloo) so the multi-rank
+    # code path can be exercised on a one-GPU box; the driver's runs use one GPU per rank over NCCL
+    if os.environ.get("QT_BENCH_ONE_GPU"):
+        local_rank = 0
 
     if args.impl == "reference":
         out = run_reference(args, rank, world)
@@ -470,7 +478,11 @@ def main():
         import torch
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("QT_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     out = run_ours(args, rank, world, local_rank)
     if not args.no_train:
         tr = run_train(rank, world, local_rank)
