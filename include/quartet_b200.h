@@ -187,11 +187,15 @@ QT_API void qt_debug_set_quant(int mode, int* fallbacks);
  *   cos/sin tables [seq, head_dim]; backward != 0 applies the transposed rotation (dx from dy).
  * qt_swiglu: forward out0 = silu(gate) * up; backward (dy given) out0 = d gate, out1 = d up.  n % 8 == 0.
  * qt_rmsnorm: rows of x [rows, d] bf16 (d % 256 == 0, d <= 2048), fp32 weight w: forward out = x rstd w and
- *   rstd[rows] saved; backward (dy, rstd given) out = dx, dw[d] += sum over rows (caller zeroes dw). */
+ *   rstd[rows] saved; backward (dy, rstd given) out = dx, dw[d] += sum over rows (caller zeroes dw).
+ * qt_cross_entropy: rows of logits [rows, vocab] bf16 (vocab % 8 == 0), int64 targets: forward writes lse and
+ *   the per-row loss (fp32); backward writes dlogits = (softmax - onehot) * (*dloss) * scale (bf16). */
 QT_API int qt_rope(const void* x, void* out, int64_t rows, int heads, int head_dim, int seq, const void* cos,
                    const void* sin, int backward, void* stream);
 QT_API int qt_rmsnorm(const void* x, const float* w, const void* dy, void* out, float* rstd, float* dw, int64_t rows,
                       int d, float eps, int backward, void* stream);
+QT_API int qt_cross_entropy(const void* logits, const int64_t* targets, int64_t rows, int vocab, float* lse,
+                            float* loss, void* dlogits, const float* dloss, float scale, int backward, void* stream);
 QT_API int qt_swiglu(const void* gate, const void* up, const void* dy, void* out0, void* out1, int64_t n,
                      int backward, void* stream);
 

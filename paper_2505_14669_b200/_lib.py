@@ -34,6 +34,7 @@ SIGNATURES = {
     "qt_debug_set_quant": (None, [_i32, _vp]),
     "qt_rope": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _vp]),
     "qt_swiglu": (_i32, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp]),
+    "qt_cross_entropy": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _f32, _i32, _vp]),
     "qt_rmsnorm": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _f32, _i32, _vp]),
     "qt_fwht32": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _f32, _vp]),
     "qt_quant_rows": (_i32, [_vp, _i32, _i64, _i64, _i64, _i32, _vp, _f32, _i32, _u64, _u64, _i64,

@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <math.h>
 
 #include "../../include/quartet_b200.h"
 
@@ -190,6 +191,78 @@ __global__ void k_rmsnorm(const uint4* __restrict__ x, const float* __restrict__
     }
 }
 
+// Cross-entropy over rows of logits [rows, V] bf16 (V % 8 == 0), one 256-thread block per row.
+// forward: online max / sum-exp in one pass -> lse[r] and loss[r] = lse - logit[target] (fp32);
+// backward: dlogits = (exp(x - lse) - [j == target]) * (*dloss) * scale, one read + one write.
+__device__ __forceinline__ void ce_merge(float& m, float& s, float m2, float s2) {
+    const float mn = fmaxf(m, m2);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
+    m = mn;
+}
+__global__ void k_xent(const uint4* __restrict__ logits, const int64_t* __restrict__ tgt, float* __restrict__ lse,
+                       float* __restrict__ loss, uint4* __restrict__ dlogits, const float* __restrict__ dloss,
+                       float scale, int64_t rows, int V, int backward) {
+    __shared__ float sm[32], ss[32];
+    const int V8 = V / 8;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const uint4* row = logits + r * V8;
+        const int64_t t = tgt[r];
+        if (!backward) {
+            float m = -INFINITY, sum = 0.f;
+            for (int i = threadIdx.x; i < V8; i += blockDim.x) {
+                const uint4 c = row[i];
+                const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+                float v[8], cm = -INFINITY;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    v[k] = bf(w[k >> 1], k & 1);
+                    cm = fmaxf(cm, v[k]);
+                }
+                float cs = 0.f;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) cs += __expf(v[k] - cm);
+                ce_merge(m, sum, cm, cs);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+                ce_merge(m, sum, m2, s2);
+            }
+            const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+            if ((threadIdx.x & 31) == 0) {
+                sm[wid] = m;
+                ss[wid] = sum;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                float M = sm[0], S = ss[0];
+                for (int k = 1; k < nw; ++k) ce_merge(M, S, sm[k], ss[k]);
+                const float l = M + __logf(S);
+                lse[r] = l;
+                const uint32_t tw = reinterpret_cast<const uint32_t*>(row)[t >> 1];
+                loss[r] = l - bf(tw, (int)(t & 1));
+            }
+            __syncthreads();
+        } else {
+            const float l = lse[r], g = *dloss * scale;
+            uint4* drow = dlogits + r * V8;
+            for (int i = threadIdx.x; i < V8; i += blockDim.x) {
+                const uint4 c = row[i];
+                const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+                uint32_t o[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t j0 = (int64_t)i * 8 + 2 * k;
+                    const float p0 = __expf(bf(w[k], 0) - l) - (j0 == t ? 1.f : 0.f);
+                    const float p1 = __expf(bf(w[k], 1) - l) - (j0 + 1 == t ? 1.f : 0.f);
+                    o[k] = pack_bf2(p0 * g, p1 * g);
+                }
+                drow[i] = make_uint4(o[0], o[1], o[2], o[3]);
+            }
+        }
+    }
+}
+
 int grid_for(int64_t work) {
     static int sms = 0;
     if (!sms) {
@@ -244,6 +317,21 @@ QT_API int qt_rmsnorm(const void* x, const float* w, const void* dy, void* out, 
         case 7: go(k_rmsnorm<7>); break;
         default: go(k_rmsnorm<8>); break;
     }
+    return (int)cudaGetLastError();
+}
+
+QT_API int qt_cross_entropy(const void* logits, const int64_t* targets, int64_t rows, int vocab, float* lse,
+                            float* loss, void* dlogits, const float* dloss, float scale, int backward, void* stream) {
+    if (rows < 0 || vocab <= 0 || vocab % 8 != 0) return QT_ERR_SHAPE;
+    if (!al16(logits) || (backward && !al16(dlogits))) return QT_ERR_ALIGN;
+    if (rows == 0) return 0;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t blocks = rows < (int64_t)sms * 8 ? rows : (int64_t)sms * 8;
+    k_xent<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint4*>(logits), targets, lse, loss,
+                                                               static_cast<uint4*>(dlogits), dloss, scale, rows,
+                                                               vocab, backward);
     return (int)cudaGetLastError();
 }
 

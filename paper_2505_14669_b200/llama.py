@@ -159,6 +159,39 @@ class _SwiGLU(torch.autograd.Function):
         return dg, du
 
 
+class _CrossEntropy(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, logits, targets):
+        logits, targets = logits.contiguous(), targets.contiguous().to(torch.int64)
+        rows, vocab = logits.shape
+        lse = torch.empty(rows, dtype=torch.float32, device=logits.device)
+        loss = torch.empty(rows, dtype=torch.float32, device=logits.device)
+        _lib.check(_lib.load().qt_cross_entropy(logits.data_ptr(), targets.data_ptr(), rows, vocab, lse.data_ptr(),
+                                                loss.data_ptr(), None, None, 1.0, 0, _stream(logits.device)),
+                   "qt_cross_entropy")
+        ctx.save_for_backward(logits, targets, lse)
+        return loss.mean()
+
+    @staticmethod
+    def backward(ctx, g):
+        logits, targets, lse = ctx.saved_tensors
+        rows, vocab = logits.shape
+        g = g.detach().to(torch.float32).contiguous()
+        d = torch.empty_like(logits)
+        _lib.check(_lib.load().qt_cross_entropy(logits.data_ptr(), targets.data_ptr(), rows, vocab, lse.data_ptr(),
+                                                None, d.data_ptr(), g.data_ptr(), 1.0 / rows, 1,
+                                                _stream(logits.device)), "qt_cross_entropy")
+        return d, None
+
+
+def cross_entropy(logits, targets):
+    """Mean cross-entropy of bf16 logits [rows, vocab] (vocab % 8 == 0): one pass forward (online
+    log-sum-exp), one pass backward (softmax - onehot); torch's F.cross_entropy otherwise."""
+    if logits.dtype == torch.bfloat16 and logits.shape[-1] % 8 == 0:
+        return _CrossEntropy.apply(logits, targets)
+    return F.cross_entropy(logits.float(), targets)
+
+
 def swiglu(g, u):
     """silu(g) * u, fused forward and backward (bf16)."""
     return _SwiGLU.apply(g, u)
@@ -350,7 +383,7 @@ class Trainer:
         for gr in self.opt.param_groups:
             gr["lr"] = lr
         logits = self.model(tokens)
-        loss = F.cross_entropy(logits.view(-1, logits.shape[-1]), targets.reshape(-1))
+        loss = cross_entropy(logits.view(-1, logits.shape[-1]), targets.reshape(-1))
         self.opt.zero_grad(set_to_none=False)
         loss.backward()                # bucket all-reduces start inside backward (hooks)
         self.bucket.finish()

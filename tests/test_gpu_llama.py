@@ -108,3 +108,17 @@ def test_fused_rmsnorm_matches_fp32_reference(llama):
     dxf, dwf = torch.autograd.grad(yf, (xf, wf), dy.float())
     torch.testing.assert_close(dx.float(), dxf, rtol=2 ** -7, atol=1e-4)
     torch.testing.assert_close(dw, dwf, rtol=1e-4, atol=1e-3)
+
+
+def test_fused_cross_entropy_matches_fp32_reference(llama):
+    """csrc/glue.cu cross-entropy (loss and dlogits) vs torch's fp32 cross-entropy on the same bf16 logits."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    logits = (torch.randn(300, 4000, device="cuda", generator=g) * 3).to(torch.bfloat16).requires_grad_(True)
+    tgt = torch.randint(0, 4000, (300,), device="cuda", generator=g)
+    loss = llama.cross_entropy(logits, tgt)
+    lf = logits.detach().float().requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(lf, tgt)
+    torch.testing.assert_close(loss, ref, rtol=1e-5, atol=1e-5)
+    (gl,) = torch.autograd.grad(loss * 2.5, logits)
+    (gr,) = torch.autograd.grad(ref * 2.5, lf)
+    torch.testing.assert_close(gl.float(), gr, rtol=2 ** -7, atol=1e-6)
