@@ -26,7 +26,7 @@ import torch.nn.functional as F
 
 from . import _lib
 from .mxfp4 import _stream
-from .nn import QuartetLinear
+from .nn import QuartetLinear, quartet_linear_group
 
 GROUP = 32
 
@@ -220,13 +220,15 @@ class Block(torch.nn.Module):
         B, S, d = x.shape
         H, dh = self.n_head, d // self.n_head
         a = self.attn_norm(x)
-        q = rope(self.q(a).view(B, S, H, dh), cos, sin).transpose(1, 2)
-        k = rope(self.k(a).view(B, S, H, dh), cos, sin).transpose(1, 2)
-        v = self.v(a).view(B, S, H, dh).transpose(1, 2)
+        q, k, v = quartet_linear_group(a, (self.q, self.k, self.v))  # one QuEST read of a for q/k/v
+        q = rope(q.view(B, S, H, dh), cos, sin).transpose(1, 2)
+        k = rope(k.view(B, S, H, dh), cos, sin).transpose(1, 2)
+        v = v.view(B, S, H, dh).transpose(1, 2)
         att = F.scaled_dot_product_attention(q, k, v, is_causal=True)
         x = x + self.o(att.transpose(1, 2).reshape(B, S, d))
         m = self.mlp_norm(x)
-        return x + self.down(swiglu(self.gate(m), self.up(m)))
+        g, u = quartet_linear_group(m, (self.gate, self.up))
+        return x + self.down(swiglu(g, u))
 
 
 class LlamaQuartet(torch.nn.Module):

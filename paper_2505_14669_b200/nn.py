@@ -58,6 +58,66 @@ class QuartetLinearFn(torch.autograd.Function):
         return dx.reshape(ctx.x_shape), dw.to(ctx.w_dtype), None, None, None, None
 
 
+class QuartetLinearGroupFn(torch.autograd.Function):
+    """Several Quartet linears reading the same x (q/k/v, gate/up): X_q and M_x = QuEST(H32 x) are computed
+    once (they depend on x alone), each layer derives its own X_t (its own xi) from X_q's codes, and the
+    input gradients of the layers are summed in x's dtype (as autograd accumulates separate layers' dx).
+    Outputs and weight gradients are bit-identical to separate QuartetLinearFn calls."""
+
+    @staticmethod
+    def forward(ctx, x, xis, rounding, hadamard, scheme, *ws):
+        lead = x.shape[:-1]
+        x2 = x.reshape(-1, x.shape[-1])
+        if x2.dtype not in (torch.bfloat16, torch.float32):
+            x2 = x2.float()
+        from .dp import ShardContext
+
+        x_q = qlinear.quantize_operand(x2, scheme, hadamard)
+        out_dtype = x.dtype if x.dtype in (torch.bfloat16, torch.float32) else torch.float32
+        ys, ctx.lctxs = [], []
+        for w, xi in zip(ws, xis):
+            y, lctx = qlinear.forward(x2, w.detach(), scheme=scheme, hadamard=hadamard, out_dtype=out_dtype,
+                                      check_finite=False, bwd_xi=int(xi), bwd_rounding=rounding,
+                                      token_offset=ShardContext.offset, total_tokens=ShardContext.total, x_q=x_q)
+            ys.append(y.reshape(*lead, w.shape[0]))
+            ctx.lctxs.append(lctx)
+        ctx.xis, ctx.rounding, ctx.x_shape, ctx.x_dtype = [int(v) for v in xis], rounding, x.shape, x.dtype
+        ctx.w_dtypes = [w.dtype for w in ws]
+        return tuple(ys)
+
+    @staticmethod
+    def backward(ctx, *dys):
+        from .dp import ShardContext
+
+        dx_dtype = ctx.x_dtype if ctx.x_dtype in (torch.bfloat16, torch.float32) else torch.float32
+        dx_sum, dws = None, []
+        for dy, lctx, xi, wdt in zip(dys, ctx.lctxs, ctx.xis, ctx.w_dtypes):
+            dy2 = dy.reshape(-1, dy.shape[-1])
+            if dy2.dtype not in (torch.bfloat16, torch.float32):
+                dy2 = dy2.float()
+            dx, dw = qlinear.backward(dy2.contiguous(), lctx, xi, ctx.rounding, dx_dtype=dx_dtype,
+                                      dw_dtype=torch.float32, check_finite=False, token_offset=ShardContext.offset,
+                                      total_tokens=ShardContext.total)
+            dx_sum = dx if dx_sum is None else dx_sum.add_(dx)  # in x's dtype, as autograd would accumulate
+            dws.append(dw.to(wdt))
+        ctx.lctxs = None
+        return (dx_sum.reshape(ctx.x_shape), None, None, None, None, *dws)
+
+
+def quartet_linear_group(x, mods):
+    """Apply QuartetLinear modules that share the input x with one forward quantization of x."""
+    m0 = mods[0]
+    if (m0.scheme.kind == "sr_absmax" or any(m.rounding != m0.rounding or m.hadamard != m0.hadamard
+                                             or m.scheme is not m0.scheme for m in mods)):
+        return tuple(m(x) for m in mods)
+    xis = []
+    for m in mods:
+        xis.append(m.xi())
+        if m.training:
+            m.step += 1
+    return QuartetLinearGroupFn.apply(x, xis, m0.rounding, m0.hadamard, m0.scheme, *[m.weight for m in mods])
+
+
 def quartet_linear(x, w, xi: int, rounding: str = "rtn", hadamard: bool = True,
                    scheme: qlinear.QuantScheme = qlinear.QUEST):
     return QuartetLinearFn.apply(x, w, xi, rounding, hadamard, scheme)

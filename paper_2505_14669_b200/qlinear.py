@@ -164,8 +164,12 @@ def quantize_operand(m: torch.Tensor, scheme: QuantScheme, hadamard: bool, seed:
 def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, policy: GemmPolicy = DEFAULT_POLICY,
             hadamard: bool = True, seed: int | None = None, out_dtype: torch.dtype = torch.float32,
             check_finite: bool = True, bwd_xi: int | None = None, bwd_rounding: str = "rtn", token_offset: int = 0,
-            total_tokens: int | None = None):
+            total_tokens: int | None = None, x_q: MXOperand | None = None):
     """y = x @ w.T through the quantized pipeline; returns (y, context)  (qlinear.py:114-165).
+
+    ``x_q``: the forward operand of x (``quantize_operand(x, ...)``) when several layers read the same x
+    (q/k/v, gate/up): X_q and its trust mask depend on x alone, so they are computed once; each layer then
+    derives its own X_t from X_q's codes (its own signs), exactly as backward does without eager operands.
 
     B200 extension: when the backward seed is already known (the training loop derives it per step and
     layer, train.py:346-348), pass it as ``bwd_xi`` (with the backward ``bwd_rounding`` and, for a
@@ -190,7 +194,31 @@ def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, polic
         sw = derive_seed(seed, _TAG_FWD_W)
     err = _err_flag(x.device) if check_finite else None
     eager = None
-    if bwd_xi is not None and bwd_rounding in ("rtn", "sr") and batch % g == 0 and d_out % g == 0:
+    if x_q is not None:
+        if x_q.rows != batch or x_q.cols != d_in:
+            raise ValueError("shared x_q does not match x")
+        if bwd_xi is not None and bwd_rounding in ("rtn", "sr") and batch % g == 0 and d_out % g == 0:
+            total = batch if total_tokens is None else int(total_tokens)
+            if token_offset % g or token_offset < 0 or token_offset + batch > total:
+                raise ValueError(f"token shard [{token_offset}, +{batch}) invalid for {total} tokens (block {g})")
+            rc = _rounding_code(bwd_rounding)
+            sr = bwd_rounding == "sr"
+            row_rc = {"quest": _lib.QT_ROUND_QUEST, "rtn_absmax": _lib.QT_ROUND_RTN,
+                      "sr_absmax": _lib.QT_ROUND_SR}[scheme.kind]
+            fwd_t = _lib.QT_TRANSFORM_HADAMARD if hadamard else _lib.QT_TRANSFORM_NONE
+            bwd_t = _lib.QT_TRANSFORM_RANDOMIZED if hadamard else _lib.QT_TRANSFORM_NONE
+            d_signs = sign_bits(bwd_xi, d_out, x.device) if hadamard else None
+            t_signs = sign_bits(bwd_xi, batch, x.device, start=token_offset) if hadamard else None
+            xt_q = quant_cols(x_q, rc, transform=bwd_t, signs=t_signs, prescale=PRE_SCALE,
+                              sr_seed=derive_seed(bwd_xi, _TAG_BWD_X) if sr else 0,
+                              counter_start=token_offset, counter_ld=total, err=err)
+            w_q, wt_q = quant_fused(w, row_rc, rc, transform=fwd_t, col_transform=bwd_t, col_signs=d_signs,
+                                    col_prescale=PRE_SCALE, sr_seed=sw or 0,
+                                    col_seed=derive_seed(bwd_xi, _TAG_BWD_W) if sr else 0, err=err)
+            eager = _Eager(int(bwd_xi), bwd_rounding, int(token_offset), total, xt_q, wt_q, d_signs, t_signs)
+        else:
+            w_q = quantize_operand(w, scheme, hadamard, sw, err)
+    elif bwd_xi is not None and bwd_rounding in ("rtn", "sr") and batch % g == 0 and d_out % g == 0:
         total = batch if total_tokens is None else int(total_tokens)
         if token_offset % g or token_offset < 0 or token_offset + batch > total:
             raise ValueError(f"token shard [{token_offset}, +{batch}) invalid for {total} tokens (block {g})")

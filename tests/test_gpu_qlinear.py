@@ -156,3 +156,31 @@ def test_autograd_function_and_module(qt):
     xi = qt.derive_seed(qt.derive_seed(3, 4, 0), 1)
     y2 = qt.quartet_linear(x2, layer.weight, xi)
     assert torch.equal(y2, y_ref)
+
+
+def test_group_of_linears_sharing_x_matches_separate_layers():
+    """quartet_linear_group (one QuEST read of x for q/k/v-style layers) gives bit-identical outputs and
+    weight gradients to separate QuartetLinear calls; dx agrees to bf16 rounding of the summed gradient."""
+    import paper_2505_14669_b200 as qt
+    from paper_2505_14669_b200.nn import QuartetLinear, quartet_linear_group
+
+    qt.load()
+    torch.manual_seed(0)
+    mods_a = [QuartetLinear(256, o, seed=3, layer_id=i, device="cuda") for i, o in enumerate((256, 128, 384))]
+    mods_b = [QuartetLinear(256, o, seed=3, layer_id=i, device="cuda") for i, o in enumerate((256, 128, 384))]
+    for a, b in zip(mods_a, mods_b):
+        b.weight.data.copy_(a.weight.data)
+    x = torch.randn(512, 256, device="cuda").to(torch.bfloat16)
+    xa, xb = x.clone().requires_grad_(True), x.clone().requires_grad_(True)
+    ya = [m(xa) for m in mods_a]
+    yb = quartet_linear_group(xb, mods_b)
+    dys = [torch.randn_like(y) for y in ya]
+    torch.autograd.backward(ya, dys)
+    torch.autograd.backward(list(yb), dys)
+    for y1, y2 in zip(ya, yb):
+        assert torch.equal(y1, y2)
+    for a, b in zip(mods_a, mods_b):
+        assert torch.equal(a.weight.grad, b.weight.grad)
+    # both sum three bf16 dx in bf16; the summation order may differ -- agreement to bf16 rounding
+    scale = xb.grad.float().abs().max()
+    assert (xa.grad.float() - xb.grad.float()).abs().max() <= 2 ** -7 * scale
