@@ -158,7 +158,8 @@ def test_autograd_function_and_module(qt):
     assert torch.equal(y2, y_ref)
 
 
-def test_group_of_linears_sharing_x_matches_separate_layers():
+@pytest.mark.parametrize("rounding", ["rtn", "sr"])
+def test_group_of_linears_sharing_x_matches_separate_layers(rounding):
     """quartet_linear_group (one QuEST read of x for q/k/v-style layers) gives bit-identical outputs and
     weight gradients to separate QuartetLinear calls; dx agrees to bf16 rounding of the summed gradient."""
     import paper_2505_14669_b200 as qt
@@ -166,8 +167,10 @@ def test_group_of_linears_sharing_x_matches_separate_layers():
 
     qt.load()
     torch.manual_seed(0)
-    mods_a = [QuartetLinear(256, o, seed=3, layer_id=i, device="cuda") for i, o in enumerate((256, 128, 384))]
-    mods_b = [QuartetLinear(256, o, seed=3, layer_id=i, device="cuda") for i, o in enumerate((256, 128, 384))]
+    mods_a = [QuartetLinear(256, o, seed=3, layer_id=i, rounding=rounding, device="cuda")
+              for i, o in enumerate((256, 128, 384))]
+    mods_b = [QuartetLinear(256, o, seed=3, layer_id=i, rounding=rounding, device="cuda")
+              for i, o in enumerate((256, 128, 384))]
     for a, b in zip(mods_a, mods_b):
         b.weight.data.copy_(a.weight.data)
     x = torch.randn(512, 256, device="cuda").to(torch.bfloat16)
