@@ -183,15 +183,16 @@ QT_API void qt_debug_set_gemm(int dbg);
 QT_API void qt_debug_set_quant(int mode, int* fallbacks);
 
 /* ---- Llama-loop glue (not on the Quartet path; llama.py): fused bf16 elementwise kernels, fp32 math.
- * qt_rope: half-split rotary embedding of x [rows, heads, head_dim] (row r at position r % seq) with
- *   cos/sin tables [seq, head_dim]; backward != 0 applies the transposed rotation (dx from dy).
+ * qt_rope: half-split rotary embedding of x [batch, seq, heads, head_dim] (rows = batch * seq; element
+ *   strides stride_b / stride_s / stride_h, head_dim contiguous) with cos/sin tables [seq, head_dim], into a
+ *   contiguous out; backward != 0 applies the transposed rotation (dx from dy).
  * qt_swiglu: forward out0 = silu(gate) * up; backward (dy given) out0 = d gate, out1 = d up.  n % 8 == 0.
  * qt_rmsnorm: rows of x [rows, d] bf16 (d % 256 == 0, d <= 2048), fp32 weight w: forward out = x rstd w and
  *   rstd[rows] saved; backward (dy, rstd given) out = dx, dw[d] += sum over rows (caller zeroes dw).
  * qt_cross_entropy: rows of logits [rows, vocab] bf16 (vocab % 8 == 0), int64 targets: forward writes lse and
  *   the per-row loss (fp32); backward writes dlogits = (softmax - onehot) * (*dloss) * scale (bf16). */
 QT_API int qt_rope(const void* x, void* out, int64_t rows, int heads, int head_dim, int seq, const void* cos,
-                   const void* sin, int backward, void* stream);
+                   const void* sin, int backward, int64_t stride_b, int64_t stride_s, int64_t stride_h, void* stream);
 QT_API int qt_rmsnorm(const void* x, const float* w, const void* dy, void* out, float* rstd, float* dw, int64_t rows,
                       int d, float eps, int backward, void* stream);
 QT_API int qt_cross_entropy(const void* logits, const int64_t* targets, int64_t rows, int vocab, float* lse,

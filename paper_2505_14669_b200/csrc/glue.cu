@@ -22,7 +22,8 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
 // tables cos/sin [S, dh].  Each thread rotates 8 (j, j + dh/2) pairs.  Backward applies the transposed
 // rotation to dy.
 __global__ void k_rope(const uint4* __restrict__ x, uint4* __restrict__ out, const uint4* __restrict__ cs,
-                       const uint4* __restrict__ sn, int64_t rows, int H, int dh, int S, int backward) {
+                       const uint4* __restrict__ sn, int64_t rows, int H, int dh, int S, int backward, int64_t sb,
+                       int64_t ss, int64_t sh) {
     const int half8 = dh / 16;                          // uint4 chunks per half row
     const int64_t total = rows * H * half8;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -30,8 +31,10 @@ __global__ void k_rope(const uint4* __restrict__ x, uint4* __restrict__ out, con
         const int64_t rh = i / half8;                   // (row, head)
         const int64_t row = rh / H;
         const int pos = (int)(row % S);
-        const int64_t base = rh * (dh / 8);             // uint4 index of this (row, head)
-        const uint4 a = x[base + c], b = x[base + half8 + c];
+        const int64_t base = rh * (dh / 8);             // uint4 index of this (row, head) in the output
+        // input element (b, s, h, :) at b sb + s ss + h sh (uint4 units; dh contiguous)
+        const int64_t ib = (row / S) * sb + (int64_t)pos * ss + (rh % H) * sh;
+        const uint4 a = x[ib + c], b = x[ib + half8 + c];
         const uint4 ca = cs[(int64_t)pos * (dh / 8) + c], cb = cs[(int64_t)pos * (dh / 8) + half8 + c];
         const uint4 sa = sn[(int64_t)pos * (dh / 8) + c], sb = sn[(int64_t)pos * (dh / 8) + half8 + c];
         const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
@@ -281,14 +284,16 @@ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 extern "C" {
 
 QT_API int qt_rope(const void* x, void* out, int64_t rows, int heads, int head_dim, int seq, const void* cos,
-                   const void* sin, int backward, void* stream) {
-    if (rows < 0 || heads <= 0 || head_dim % 16 != 0 || seq <= 0) return QT_ERR_SHAPE;
-    if (!al16(x) || !al16(out) || !al16(cos) || !al16(sin)) return QT_ERR_ALIGN;
+                   const void* sin, int backward, int64_t stride_b, int64_t stride_s, int64_t stride_h, void* stream) {
+    if (rows < 0 || heads <= 0 || head_dim % 16 != 0 || seq <= 0 || rows % seq != 0) return QT_ERR_SHAPE;
+    if (!al16(x) || !al16(out) || !al16(cos) || !al16(sin) || stride_b % 8 || stride_s % 8 || stride_h % 8)
+        return QT_ERR_ALIGN;
     const int64_t work = rows * heads * (head_dim / 16);
     if (work == 0) return 0;
     k_rope<<<grid_for(work), 256, 0, (cudaStream_t)stream>>>(
         static_cast<const uint4*>(x), static_cast<uint4*>(out), static_cast<const uint4*>(cos),
-        static_cast<const uint4*>(sin), rows, heads, head_dim, seq, backward);
+        static_cast<const uint4*>(sin), rows, heads, head_dim, seq, backward, stride_b / 8, stride_s / 8,
+        stride_h / 8);
     return (int)cudaGetLastError();
 }
 

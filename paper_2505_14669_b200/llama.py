@@ -119,11 +119,15 @@ def _apply_rope_torch(x, cos, sin):  # x [B, H, S, dh] bf16 (reference formulati
 
 
 def _rope_call(x, cos, sin, backward: bool):
-    """x [B, S, H, dh] contiguous bf16 -> rotated copy (csrc/glue.cu, one pass)."""
+    """x [B, S, H, dh] bf16 (any strides with dh contiguous, e.g. the transposed gradient of attention) ->
+    rotated contiguous copy (csrc/glue.cu, one pass)."""
     B, S, H, dh = x.shape
-    out = torch.empty_like(x)
+    if x.stride(3) != 1 or any(st % 8 for st in x.stride()[:3]) or x.data_ptr() % 16:
+        x = x.contiguous()
+    out = torch.empty((B, S, H, dh), dtype=x.dtype, device=x.device)
     _lib.check(_lib.load().qt_rope(x.data_ptr(), out.data_ptr(), B * S, H, dh, S, cos.data_ptr(), sin.data_ptr(),
-                                   int(backward), _stream(x.device)), "qt_rope")
+                                   int(backward), x.stride(0), x.stride(1), x.stride(2), _stream(x.device)),
+               "qt_rope")
     return out
 
 
@@ -131,12 +135,12 @@ class _Rope(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, cos, sin):
         ctx.save_for_backward(cos, sin)
-        return _rope_call(x.contiguous(), cos, sin, False)
+        return _rope_call(x, cos, sin, False)
 
     @staticmethod
     def backward(ctx, dy):
         cos, sin = ctx.saved_tensors
-        return _rope_call(dy.contiguous(), cos, sin, True), None, None
+        return _rope_call(dy, cos, sin, True), None, None
 
 
 class _SwiGLU(torch.autograd.Function):

@@ -122,3 +122,17 @@ def test_fused_cross_entropy_matches_fp32_reference(llama):
     (gl,) = torch.autograd.grad(loss * 2.5, logits)
     (gr,) = torch.autograd.grad(ref * 2.5, lf)
     torch.testing.assert_close(gl.float(), gr, rtol=2 ** -7, atol=1e-6)
+
+
+def test_fused_rope_strided_input(llama):
+    """The rotary kernel reads a non-contiguous [B, S, H, dh] view (attention's transposed gradient layout)
+    directly; result equal to rotating the contiguous copy."""
+    B, S, H, dh = 2, 64, 4, 128
+    cos, sin = llama._rope(S, dh, 10000.0, "cuda")
+    base = torch.randn(B, H, S, dh, device="cuda").to(torch.bfloat16)
+    xv = base.transpose(1, 2)                    # [B, S, H, dh], non-contiguous
+    assert not xv.is_contiguous()
+    for bwd in (False, True):
+        a = llama._rope_call(xv, cos, sin, bwd)
+        b = llama._rope_call(xv.contiguous(), cos, sin, bwd)
+        assert torch.equal(a, b)
