@@ -6,7 +6,8 @@ import paper_2505_14669_b200 as qt
 from paper_2505_14669_b200 import _lib
 from paper_2505_14669_b200.mxfp4 import quant_fused, quant_rows, sign_bits
 L = qt.load()
-x = torch.randn(16384, 4096, device="cuda").to(torch.bfloat16)
+C = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+x = torch.randn(16384, C, device="cuda").to(torch.bfloat16)
 s = sign_bits(3, 16384, "cuda")
 H, RT, Q, RTN = _lib.QT_TRANSFORM_HADAMARD, _lib.QT_TRANSFORM_RANDOMIZED, _lib.QT_ROUND_QUEST, _lib.QT_ROUND_RTN
 def t(f, n=10):
