@@ -368,7 +368,7 @@ def run_ours(args, rank, world, local_rank):
         "kernels": table,
         "e2e": e2e,
         # per step and shape: 2 sign bitmaps + 2 fused forward quantizers + 1 GEMM; 1 dual quantizer + 2 GEMMs
-        "gpu_launches": 8 * len(SHAPES) * args.steps,
+        "gpu_launches": 7 * len(SHAPES) * args.steps,  # signs pair, fused X, fused W, GEMM, dual dy, 2 GEMMs
         "clocks": clocks,
     }
 

@@ -85,6 +85,10 @@ QT_API uint64_t qt_derive_seed(const uint64_t* parts, int nparts);      /* rng.d
 QT_API int qt_sign_bits(uint32_t* d_bits, int64_t n, uint64_t xi, void* stream);
 /* Same for rng.signs(xi, start, n): positions start .. start+n-1 (data-parallel token shards). */
 QT_API int qt_sign_bits_at(uint32_t* d_bits, int64_t start, int64_t n, uint64_t xi, void* stream);
+/* Both sign vectors of one seed in one launch: rng.signs(xi, start_a, n_a) into a, rng.signs(xi, start_b, n_b)
+ * into b (a layer's d_out and token signs; same bitmaps as two qt_sign_bits_at calls). */
+QT_API int qt_sign_bits_pair(uint32_t* a, int64_t start_a, int64_t n_a, uint32_t* b, int64_t start_b, int64_t n_b,
+                             uint64_t xi, void* stream);
 
 /* Blockwise transform only (the kernels.fwht plugin entry, _native.pyx:353-379, with the
  * randomized variant of hadamard.py:82-85): out[r, :] = prescale * FWHT32(x[r, :] (.) s), fp32,

@@ -64,6 +64,12 @@ int qt_sign_bits_at(uint32_t* d_bits, int64_t start, int64_t n, uint64_t xi, voi
     return launch_signs(d_bits, start, n, xi, (cudaStream_t)stream);
 }
 
+int qt_sign_bits_pair(uint32_t* a, int64_t start_a, int64_t n_a, uint32_t* b, int64_t start_b, int64_t n_b,
+                      uint64_t xi, void* stream) {
+    if (start_a < 0 || start_b < 0 || n_a < 0 || n_b < 0) return QT_ERR_ARG;
+    return launch_signs2(a, start_a, n_a, b, start_b, n_b, xi, (cudaStream_t)stream);
+}
+
 int qt_fwht32(const float* x, float* out, int64_t rows, int64_t cols, int transform, const uint32_t* sign_bits,
              float prescale, void* stream) {
     if (cols % 32 != 0 || rows < 0) return QT_ERR_SHAPE;

@@ -50,6 +50,8 @@ struct EpiParams {
 int launch_transform_rows(const float* x, float* out, int64_t rows, int64_t cols, int transform,
                           const uint32_t* sign_bits, float prescale, cudaStream_t st);
 int launch_signs(uint32_t* bits, int64_t start, int64_t n, uint64_t xi, cudaStream_t st);
+int launch_signs2(uint32_t* a, int64_t sa, int64_t na, uint32_t* b, int64_t sb, int64_t nb, uint64_t xi,
+                  cudaStream_t st);
 int launch_quant_rows(const void* x, int in_type, int64_t ldx, int64_t rows, int64_t cols, const QuantCfg& cfg,
                       const QuantOut& out, cudaStream_t st);
 int launch_quant_tile(const void* x, int in_type, int64_t ldx, const MxIn& mx, int64_t R, int64_t C,

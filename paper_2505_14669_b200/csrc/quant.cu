@@ -24,6 +24,28 @@
 
 namespace qt {
 
+__device__ __forceinline__ void signs_word(uint32_t* bits, int64_t start, int64_t n, uint64_t base, int64_t w) {
+    uint32_t m = 0;
+    for (int j = 0; j < 32; ++j) {
+        const int64_t p = w * 32 + j;
+        if (p < n) {
+            const uint64_t h = mix64(base + ((uint64_t)(start + p) + 1) * kGolden);
+            m |= (uint32_t)(h >> 63) << j;
+        }
+    }
+    bits[w] = m;
+}
+// two sign vectors of one seed in one launch (a layer's d_out and token signs): blocks [0, nba) -> a
+__global__ void k_signs2(uint32_t* a, int64_t sa, int64_t na, int64_t nba, uint32_t* b, int64_t sb, int64_t nb,
+                         uint64_t base) {
+    const bool first = blockIdx.x < nba;
+    const int64_t w = (first ? blockIdx.x : blockIdx.x - nba) * (int64_t)blockDim.x + threadIdx.x;
+    if (first) {
+        if (w < (na + 31) / 32) signs_word(a, sa, na, base, w);
+    } else if (w < (nb + 31) / 32) {
+        signs_word(b, sb, nb, base, w);
+    }
+}
 __global__ void k_signs(uint32_t* bits, int64_t start, int64_t n, uint64_t base) {
     int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t nw = (n + 31) / 32;
@@ -424,6 +446,15 @@ __global__ void __launch_bounds__(256, 2) k_quant(TileArgs a) {
 
 // ------------------------------------------------------------------------------- launchers
 namespace qt {
+
+int launch_signs2(uint32_t* a, int64_t sa, int64_t na, uint32_t* b, int64_t sb, int64_t nb, uint64_t xi,
+                  cudaStream_t st) {
+    const uint64_t base = mix64(xi ^ mix64(kDomainSigns));
+    const int64_t nba = ((na + 31) / 32 + 255) / 256, nbb = ((nb + 31) / 32 + 255) / 256;
+    if (nba + nbb == 0) return 0;
+    k_signs2<<<(unsigned)(nba + nbb), 256, 0, st>>>(a, sa, na, nba, b, sb, nb, base);
+    return (int)cudaGetLastError();
+}
 
 int launch_signs(uint32_t* bits, int64_t start, int64_t n, uint64_t xi, cudaStream_t st) {
     if (n <= 0) return 0;

@@ -110,6 +110,15 @@ def sign_bits(xi: int, n: int, device, start: int = 0) -> torch.Tensor:
     return out
 
 
+def sign_bits_pair(xi: int, n_a: int, n_b: int, device, start_a: int = 0, start_b: int = 0):
+    """sign_bits(xi, n_a, start=start_a), sign_bits(xi, n_b, start=start_b) in one launch."""
+    a = torch.empty(((n_a + 31) // 32,), dtype=torch.int32, device=device)
+    b = torch.empty(((n_b + 31) // 32,), dtype=torch.int32, device=device)
+    check(_lib.load().qt_sign_bits_pair(a.data_ptr(), int(start_a), n_a, b.data_ptr(), int(start_b), n_b,
+                                        int(xi) & 0xFFFFFFFFFFFFFFFF, _stream(a.device)), "qt_sign_bits_pair")
+    return a, b
+
+
 def fwht32(x: torch.Tensor, transform: int = 1, signs: torch.Tensor | None = None,
            prescale: float = 1.0) -> torch.Tensor:
     """prescale * FWHT32(x (.) s) along the last axis, fp32 (kernels.fwht, _native.pyx:353-379)."""

@@ -28,7 +28,8 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from .mxfp4 import GROUP, MXOperand, derive_seed, gemm, quant_cols, quant_dual, quant_fused, quant_rows, sign_bits
+from .mxfp4 import (GROUP, MXOperand, derive_seed, gemm, quant_cols, quant_dual, quant_fused, quant_rows, sign_bits,
+                    sign_bits_pair)
 
 PRE_SCALE = 0.75                     # qlinear.py:36
 POST_SCALE = 16.0 / 9.0              # qlinear.py:37
@@ -207,8 +208,8 @@ def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, polic
                       "sr_absmax": _lib.QT_ROUND_SR}[scheme.kind]
             fwd_t = _lib.QT_TRANSFORM_HADAMARD if hadamard else _lib.QT_TRANSFORM_NONE
             bwd_t = _lib.QT_TRANSFORM_RANDOMIZED if hadamard else _lib.QT_TRANSFORM_NONE
-            d_signs = sign_bits(bwd_xi, d_out, x.device) if hadamard else None
-            t_signs = sign_bits(bwd_xi, batch, x.device, start=token_offset) if hadamard else None
+            d_signs, t_signs = (sign_bits_pair(bwd_xi, d_out, batch, x.device, start_b=token_offset) if hadamard
+                                else (None, None))
             xt_q = quant_cols(x_q, rc, transform=bwd_t, signs=t_signs, prescale=PRE_SCALE,
                               sr_seed=derive_seed(bwd_xi, _TAG_BWD_X) if sr else 0,
                               counter_start=token_offset, counter_ld=total, err=err)
@@ -227,8 +228,8 @@ def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, polic
         row_rc = {"quest": _lib.QT_ROUND_QUEST, "rtn_absmax": _lib.QT_ROUND_RTN, "sr_absmax": _lib.QT_ROUND_SR}[scheme.kind]
         fwd_t = _lib.QT_TRANSFORM_HADAMARD if hadamard else _lib.QT_TRANSFORM_NONE
         bwd_t = _lib.QT_TRANSFORM_RANDOMIZED if hadamard else _lib.QT_TRANSFORM_NONE
-        d_signs = sign_bits(bwd_xi, d_out, x.device) if hadamard else None
-        t_signs = sign_bits(bwd_xi, batch, x.device, start=token_offset) if hadamard else None
+        d_signs, t_signs = (sign_bits_pair(bwd_xi, d_out, batch, x.device, start_b=token_offset) if hadamard
+                            else (None, None))
         x_q, xt_q = quant_fused(x, row_rc, rc, transform=fwd_t, col_transform=bwd_t, col_signs=t_signs,
                                 col_prescale=PRE_SCALE, sr_seed=sx or 0,
                                 col_seed=derive_seed(bwd_xi, _TAG_BWD_X) if sr else 0,
@@ -290,8 +291,9 @@ def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn"
     if ea is not None:
         d_signs, t_signs = ea.d_signs, ea.t_signs
     else:
-        d_signs = sign_bits(xi, ctx.d_out, dev) if ctx.hadamard else None                       # along d_out
-        t_signs = sign_bits(xi, ctx.batch, dev, start=token_offset) if ctx.hadamard else None   # along tokens
+        # along d_out and along tokens, one launch
+        d_signs, t_signs = (sign_bits_pair(xi, ctx.d_out, ctx.batch, dev, start_b=token_offset) if ctx.hadamard
+                            else (None, None))
     sr = rounding == "sr"
     err = _err_flag(dev) if check_finite else None
 

@@ -365,3 +365,12 @@ def test_tensor_core_quest_forward_equals_exact_path(qt, case):
     assert torch.equal(c0.codes, c1.codes)
     assert torch.equal(c0.scales_rowmajor(), c1.scales_rowmajor())
     print(f"{case}: X_q / X_t groups re-decided exactly {fb.tolist()} of {R * C // 32}")
+
+
+def test_sign_bits_pair_equals_two_calls(qt):
+    from paper_2505_14669_b200.mxfp4 import sign_bits, sign_bits_pair
+
+    for n_a, n_b, s_b in [(4096, 16384, 0), (96, 160, 64), (11008, 2048, 8192), (0, 33, 5)]:
+        a, b = sign_bits_pair(12345, n_a, n_b, "cuda", start_b=s_b)
+        assert torch.equal(a, sign_bits(12345, n_a, "cuda")) if n_a else a.numel() == 0
+        assert torch.equal(b, sign_bits(12345, n_b, "cuda", start=s_b))
