@@ -18,10 +18,14 @@ for (M, N, K) in [(16384, 4096, 4096), (16384, 4096, 16384)]:
     A = qt.quant_rows(x, 0, _lib.QT_ROUND_RTN)
     B = qt.quant_rows(w, 0, _lib.QT_ROUND_RTN)
     out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
-    for dbg, name in [(0, "baseline (2-CTA pairs)"), (0x80000, "pairs in clusters of 8, multicast"), (0x40000, "1-CTA 128x256 tiles"), (0x100, "no epilogue math/stores"),
-                      (0x4000, "grouped-2 walk"), (0x1000, "grouped-4 walk"), (0x2000, "grouped-16 walk"), (1, "no SF tcgen05.cp after k0"), (3, "no SF loads+cp after k0"),
-                      (4, "1 MMA per k-tile (1/4 math)"), (8, "no B TMA after k0"), (12, "no B + 1 MMA"),
-                      (11, "no B, no SF")]:
+    # knobs 1/2/4/8 (scale copies, B loads, MMA count) exist in the 1-CTA kernel only: run them with 0x40000
+    C1 = 0x40000
+    for dbg, name in [(0, "baseline (2-CTA pairs)"), (0x80000, "pairs in clusters of 8, multicast"),
+                      (0x100, "no epilogue math/stores"), (0x4000, "grouped-2 walk"), (0x1000, "grouped-4 walk"),
+                      (0x2000, "grouped-16 walk"), (C1, "1-CTA 128x256 tiles"),
+                      (C1 | 1, "1-CTA, no SF tcgen05.cp after k0"), (C1 | 3, "1-CTA, no SF loads+cp after k0"),
+                      (C1 | 4, "1-CTA, 1 MMA per k-tile (1/4 math)"), (C1 | 8, "1-CTA, no B TMA after k0"),
+                      (C1 | 12, "1-CTA, no B + 1 MMA"), (C1 | 11, "1-CTA, no B, no SF")]:
         L.qt_debug_set_gemm(dbg)
         for _ in range(3):
             qt.gemm(A, B, out=out)
