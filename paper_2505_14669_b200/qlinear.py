@@ -195,31 +195,9 @@ def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, polic
         sw = derive_seed(seed, _TAG_FWD_W)
     err = _err_flag(x.device) if check_finite else None
     eager = None
-    if x_q is not None:
-        if x_q.rows != batch or x_q.cols != d_in:
-            raise ValueError("shared x_q does not match x")
-        if bwd_xi is not None and bwd_rounding in ("rtn", "sr") and batch % g == 0 and d_out % g == 0:
-            total = batch if total_tokens is None else int(total_tokens)
-            if token_offset % g or token_offset < 0 or token_offset + batch > total:
-                raise ValueError(f"token shard [{token_offset}, +{batch}) invalid for {total} tokens (block {g})")
-            rc = _rounding_code(bwd_rounding)
-            sr = bwd_rounding == "sr"
-            row_rc = {"quest": _lib.QT_ROUND_QUEST, "rtn_absmax": _lib.QT_ROUND_RTN,
-                      "sr_absmax": _lib.QT_ROUND_SR}[scheme.kind]
-            fwd_t = _lib.QT_TRANSFORM_HADAMARD if hadamard else _lib.QT_TRANSFORM_NONE
-            bwd_t = _lib.QT_TRANSFORM_RANDOMIZED if hadamard else _lib.QT_TRANSFORM_NONE
-            d_signs, t_signs = (sign_bits_pair(bwd_xi, d_out, batch, x.device, start_b=token_offset) if hadamard
-                                else (None, None))
-            xt_q = quant_cols(x_q, rc, transform=bwd_t, signs=t_signs, prescale=PRE_SCALE,
-                              sr_seed=derive_seed(bwd_xi, _TAG_BWD_X) if sr else 0,
-                              counter_start=token_offset, counter_ld=total, err=err)
-            w_q, wt_q = quant_fused(w, row_rc, rc, transform=fwd_t, col_transform=bwd_t, col_signs=d_signs,
-                                    col_prescale=PRE_SCALE, sr_seed=sw or 0,
-                                    col_seed=derive_seed(bwd_xi, _TAG_BWD_W) if sr else 0, err=err)
-            eager = _Eager(int(bwd_xi), bwd_rounding, int(token_offset), total, xt_q, wt_q, d_signs, t_signs)
-        else:
-            w_q = quantize_operand(w, scheme, hadamard, sw, err)
-    elif bwd_xi is not None and bwd_rounding in ("rtn", "sr") and batch % g == 0 and d_out % g == 0:
+    if x_q is not None and (x_q.rows != batch or x_q.cols != d_in):
+        raise ValueError("shared x_q does not match x")
+    if bwd_xi is not None and bwd_rounding in ("rtn", "sr") and batch % g == 0 and d_out % g == 0:
         total = batch if total_tokens is None else int(total_tokens)
         if token_offset % g or token_offset < 0 or token_offset + batch > total:
             raise ValueError(f"token shard [{token_offset}, +{batch}) invalid for {total} tokens (block {g})")
@@ -230,16 +208,21 @@ def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, polic
         bwd_t = _lib.QT_TRANSFORM_RANDOMIZED if hadamard else _lib.QT_TRANSFORM_NONE
         d_signs, t_signs = (sign_bits_pair(bwd_xi, d_out, batch, x.device, start_b=token_offset) if hadamard
                             else (None, None))
-        x_q, xt_q = quant_fused(x, row_rc, rc, transform=fwd_t, col_transform=bwd_t, col_signs=t_signs,
-                                col_prescale=PRE_SCALE, sr_seed=sx or 0,
-                                col_seed=derive_seed(bwd_xi, _TAG_BWD_X) if sr else 0,
-                                col_counter_start=token_offset, col_counter_ld=total, err=err)
+        x_seed = derive_seed(bwd_xi, _TAG_BWD_X) if sr else 0
+        if x_q is None:
+            x_q, xt_q = quant_fused(x, row_rc, rc, transform=fwd_t, col_transform=bwd_t, col_signs=t_signs,
+                                    col_prescale=PRE_SCALE, sr_seed=sx or 0, col_seed=x_seed,
+                                    col_counter_start=token_offset, col_counter_ld=total, err=err)
+        else:  # shared X_q: this layer's X_t from its codes, as backward does without eager operands
+            xt_q = quant_cols(x_q, rc, transform=bwd_t, signs=t_signs, prescale=PRE_SCALE, sr_seed=x_seed,
+                              counter_start=token_offset, counter_ld=total, err=err)
         w_q, wt_q = quant_fused(w, row_rc, rc, transform=fwd_t, col_transform=bwd_t, col_signs=d_signs,
                                 col_prescale=PRE_SCALE, sr_seed=sw or 0,
                                 col_seed=derive_seed(bwd_xi, _TAG_BWD_W) if sr else 0, err=err)
         eager = _Eager(int(bwd_xi), bwd_rounding, int(token_offset), total, xt_q, wt_q, d_signs, t_signs)
     else:
-        x_q = quantize_operand(x, scheme, hadamard, sx, err)
+        if x_q is None:
+            x_q = quantize_operand(x, scheme, hadamard, sx, err)
         w_q = quantize_operand(w, scheme, hadamard, sw, err)
     y = gemm(x_q, w_q, out_dtype=out_dtype)
     _raise_if_nonfinite(err)
