@@ -308,6 +308,25 @@ __device__ __forceinline__ void load_col_codes(const uint8_t* codes, const float
     }
 }
 
+// One column c (rows 32q .. 32q+31) of the staged codes tile: the nibble c % 2 of byte pair c / 2.
+__device__ __forceinline__ void load_col_code1(const uint8_t* codes, const float* T, int tstride, int c, int q,
+                                               int transform, float (&v)[32]) {
+    const int cp = c >> 1, hi = c & 1;
+    const float4* trow = reinterpret_cast<const float4*>(T + (c >> 5) * tstride + q * 32);
+#pragma unroll
+    for (int i4 = 0; i4 < 8; ++i4) {
+        const float4 s = trow[i4];
+        const float sv[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = i4 * 4 + u, r = q * 32 + i;
+            const float2 f = e2m1x2_to_f32(codes[codes_byte(r, cp)]);
+            v[i] = __fmul_rn(hi ? f.y : f.x, sv[u]);
+        }
+    }
+    if (transform != kNone) fwht_full(v);
+}
+
 // ------------------------------------------------------------------------------- kernel
 template <int IN, int ROW, int COL, int CROUND>
 __global__ void __launch_bounds__(256, 2) k_quant(TileArgs a) {
@@ -417,7 +436,23 @@ __global__ void __launch_bounds__(256, 2) k_quant(TileArgs a) {
         }
 
         // ---------------------------------------------------------------- col pass
-        if (COL != kColOff) {
+        if (COL == kColCodes && TR == 64) {
+            // 64-row (fp32) tiles hold 2 column groups per column: one column per thread keeps all 256 threads
+            // busy (the pair layout below would leave half of them idle)
+            const int c = tid & 127, q = tid >> 7;
+            if (c < nc && q * 32 < nr) {
+                float v[32];
+                load_col_code1(codes_s, T, G::TSTRIDE, c, q, cc.transform, v);
+                const int64_t orow = c0 + c, ogrp = r0 / 32 + q;
+                const int64_t cld = cc.counter_ld ? cc.counter_ld : a.R;
+                uint4 codes;
+                uint32_t mask;
+                const int e = quant_group<CROUND>(v, cc, cc.counter_start + (uint64_t)(orow * cld + ogrp * 32),
+                                                  a.col_out.err, nullptr, codes, mask);
+                *reinterpret_cast<uint4*>(a.col_out.codes + orow * a.col_out.ldc + ogrp * 16) = codes;
+                a.col_out.sf[sf_offset(orow, ogrp, a.col_out.katoms)] = (uint8_t)e;
+            }
+        } else if (COL != kColOff) {
             const int cp = tid & 63, q = tid >> 6;
             if (q < TR / 32 && 2 * cp < nc && q * 32 < nr) {
                 float va[32], vb[32];
