@@ -266,6 +266,92 @@ __global__ void k_xent(const uint4* __restrict__ logits, const int64_t* __restri
     }
 }
 
+// Wide rows (d = 2048 * NV, one 256-thread block per row, 8 * NV elements per thread): same math as
+// k_rmsnorm; dw partials stay in registers across the block's rows, one atomic per column per block.
+template <int NV>
+__global__ void __launch_bounds__(256) k_rmsnorm_wide(const uint4* __restrict__ x, const float* __restrict__ w,
+                                                      const uint4* __restrict__ dy, uint4* __restrict__ out,
+                                                      float* __restrict__ rstd_io, float* __restrict__ dw,
+                                                      int64_t rows, float eps, int backward) {
+    constexpr int D = 2048 * NV;
+    __shared__ float red[8];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    float wv[NV][8], dwp[NV][8];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            wv[v][t] = w[(v * 256 + tid) * 8 + t];
+            dwp[v][t] = 0.f;
+        }
+    auto block_sum = [&](float val) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        __syncthreads();
+        if (lane == 0) red[wid] = val;
+        __syncthreads();
+        float tot = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) tot += red[k];
+        return tot;
+    };
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        float xv[NV][8], ss = 0.f;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const uint4 c = x[r * (D / 8) + v * 256 + tid];
+            const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                xv[v][t] = bf(cw[t >> 1], t & 1);
+                ss = fmaf(xv[v][t], xv[v][t], ss);
+            }
+        }
+        if (!backward) {
+            const float rs = rsqrtf(block_sum(ss) / (float)D + eps);
+            if (tid == 0) rstd_io[r] = rs;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                uint32_t o4[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    o4[t] = pack_bf2(xv[v][2 * t] * rs * wv[v][2 * t], xv[v][2 * t + 1] * rs * wv[v][2 * t + 1]);
+                out[r * (D / 8) + v * 256 + tid] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+            }
+        } else {
+            const float rs = rstd_io[r];
+            float gv[NV][8], dot = 0.f;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const uint4 c = dy[r * (D / 8) + v * 256 + tid];
+                const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    const float dd = bf(cw[t >> 1], t & 1), xh = xv[v][t] * rs;
+                    gv[v][t] = dd * wv[v][t];
+                    dot = fmaf(gv[v][t], xh, dot);
+                    dwp[v][t] = fmaf(dd, xh, dwp[v][t]);
+                }
+            }
+            const float mdot = block_sum(dot) / (float)D;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                uint32_t o4[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    o4[t] = pack_bf2(rs * (gv[v][2 * t] - xv[v][2 * t] * rs * mdot),
+                                     rs * (gv[v][2 * t + 1] - xv[v][2 * t + 1] * rs * mdot));
+                out[r * (D / 8) + v * 256 + tid] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+            }
+        }
+    }
+    if (backward)
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int t = 0; t < 8; ++t) atomicAdd(dw + (v * 256 + tid) * 8 + t, dwp[v][t]);
+}
+
 int grid_for(int64_t work) {
     static int sms = 0;
     if (!sms) {
@@ -299,9 +385,23 @@ QT_API int qt_rope(const void* x, void* out, int64_t rows, int heads, int head_d
 
 QT_API int qt_rmsnorm(const void* x, const float* w, const void* dy, void* out, float* rstd, float* dw, int64_t rows,
                       int d, float eps, int backward, void* stream) {
-    if (rows < 0 || d % 256 != 0 || d < 256 || d > 2048) return QT_ERR_SHAPE;
+    if (rows < 0 || d % 256 != 0 || d < 256 || (d > 2048 && (d % 2048 != 0 || d > 8192))) return QT_ERR_SHAPE;
     if (!al16(x) || !al16(out) || (backward && (!al16(dy) || !dw))) return QT_ERR_ALIGN;
     if (rows == 0) return 0;
+    if (d > 2048) {
+        int blocks = grid_for(rows * 256);
+        if (blocks > 1184) blocks = 1184;
+        auto wide = [&](auto kern) {
+            kern<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint4*>(x), w, static_cast<const uint4*>(dy),
+                                                           static_cast<uint4*>(out), rstd, dw, rows, eps, backward);
+        };
+        switch (d / 2048) {
+            case 2: wide(k_rmsnorm_wide<2>); break;
+            case 3: wide(k_rmsnorm_wide<3>); break;
+            default: wide(k_rmsnorm_wide<4>); break;
+        }
+        return (int)cudaGetLastError();
+    }
     const int warps = 8;
     int blocks = grid_for(rows * 32);
     if (blocks > 1184) blocks = 1184;

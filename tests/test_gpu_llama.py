@@ -91,11 +91,12 @@ def test_fused_swiglu_matches_fp32_reference(llama):
     torch.testing.assert_close(du.float(), duf, rtol=2 ** -7, atol=1e-4)
 
 
-def test_fused_rmsnorm_matches_fp32_reference(llama):
-    """csrc/glue.cu RMSNorm (forward, dx, dw) vs an fp32 torch reference; tolerance: bf16 rounding of the
-    outputs (2^-7 relative) and fp32 summation order for dw."""
-    x = torch.randn(1000, 1280, device="cuda").to(torch.bfloat16).requires_grad_(True)
-    norm = llama.RMSNorm(1280, device="cuda")
+@pytest.mark.parametrize("d", [1280, 4096])
+def test_fused_rmsnorm_matches_fp32_reference(llama, d):
+    """csrc/glue.cu RMSNorm (forward, dx, dw; warp-per-row and block-per-row variants) vs an fp32 torch
+    reference; tolerance: bf16 rounding of the outputs (2^-7 relative) and fp32 summation order for dw."""
+    x = torch.randn(1000, d, device="cuda").to(torch.bfloat16).requires_grad_(True)
+    norm = llama.RMSNorm(d, device="cuda")
     with torch.no_grad():
         norm.weight.uniform_(0.5, 1.5)
     y = norm(x)
