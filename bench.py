@@ -186,6 +186,78 @@ def kernel_table(qt, data, dev, reps=10):
 
 
 # ---------------------------------------------------------------------------- our arm
+def johnson_order(a, b):
+    """Two-machine flow-shop order (Johnson's rule) for jobs with upload times a and download times b:
+    jobs with a < b first by increasing a, then the rest by decreasing b."""
+    first = sorted((i for i in range(len(a)) if a[i] < b[i]), key=lambda i: a[i])
+    rest = sorted((i for i in range(len(a)) if a[i] >= b[i]), key=lambda i: -b[i])
+    return first + rest
+
+
+def e2e_pipeline(qt, data, dev, steps):
+    """End to end through the public API with host buffers: every step uploads each shape's x and dy
+    from pinned host memory and downloads its dx (bf16) and dw (fp32).  Three streams -- uploads,
+    compute, downloads -- so PCIe runs both directions at once (full duplex, measured 92 GB/s
+    aggregate vs 55 GB/s one way; tools/pcie_probe.py): shape i's upload overlaps shape i-1's
+    compute and shape i-2's download, and step k+1's uploads overlap step k's last downloads.
+    Device input buffers are double-buffered by step parity; shapes run in Johnson order
+    (upload-light / download-heavy first), which minimises the two-stage makespan."""
+    import torch
+
+    host = [(x.cpu().pin_memory(), dy.cpu().pin_memory()) for (x, _, dy) in data]
+    outs = [(torch.empty(x.shape, dtype=torch.bfloat16).pin_memory(),
+             torch.empty(w.shape, dtype=torch.float32).pin_memory()) for (x, w, _) in data]
+    bufs = [[(torch.empty_like(x), torch.empty_like(dy)) for (x, _, dy) in data] for _ in range(2)]
+    up, down = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    comp = torch.cuda.current_stream(dev)
+    freed = [[None] * len(data) for _ in range(2)]   # compute done with bufs[parity][i]
+    up_b = [hx.numel() * 2 + hdy.numel() * 2 for hx, hdy in host]
+    down_b = [ox.numel() * 2 + ow.numel() * 4 for ox, ow in outs]
+    order = johnson_order(up_b, down_b)
+
+    def e2e_step(k, xi):
+        par = k & 1
+        for i in order:
+            (hx, hdy), (ox, ow), (bx, bdy) = host[i], outs[i], bufs[par][i]
+            with torch.cuda.stream(up):
+                if freed[par][i] is not None:
+                    up.wait_event(freed[par][i])
+                bx.copy_(hx, non_blocking=True)
+                bdy.copy_(hdy, non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(up)
+            comp.wait_event(ready)
+            y, ctx = qt.forward(bx, data[i][1], out_dtype=torch.bfloat16, check_finite=False, bwd_xi=xi * 3 + i)
+            dx, dw = qt.backward(bdy, ctx, xi=xi * 3 + i, dx_dtype=torch.bfloat16, check_finite=False)
+            done = torch.cuda.Event()
+            done.record(comp)
+            freed[par][i] = done
+            with torch.cuda.stream(down):
+                down.wait_event(done)
+                ox.copy_(dx, non_blocking=True)
+                ow.copy_(dw, non_blocking=True)
+            dx.record_stream(down)
+            dw.record_stream(down)
+        return sum(up_b), sum(down_b)
+
+    for k in range(2):
+        e2e_step(k, k)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(comp)
+    for k in range(steps):
+        h2d, d2h = e2e_step(k, 100 + k)
+    comp.wait_stream(up)
+    comp.wait_stream(down)
+    e.record(comp)
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / steps
+    return {"value": round(flops_per_step(data[0][0].shape[0]) / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+            "ms_per_step": round(ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "path": "paper_2505_14669_b200.forward/backward (C ABI), eager; pinned host x/dy in, dx/dw out; "
+                    "upload / compute / download streams (PCIe full duplex), double-buffered inputs"}
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -290,36 +362,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     bf16_ms = s.elapsed_time(e) / args.steps
 
-    # end-to-end through the public API with host buffers (H2D inputs, D2H results)
-    host = [(x.cpu().pin_memory(), dy.cpu().pin_memory()) for (x, _, dy) in data]
-    outs = [(torch.empty(x.shape, dtype=torch.bfloat16).pin_memory(),
-             torch.empty(w.shape, dtype=torch.float32).pin_memory()) for (x, w, _) in data]
-
-    def e2e_step(xi):
-        h2d = d2h = 0
-        for i, ((hx, hdy), (_, w_dev, _), (ox, ow)) in enumerate(zip(host, data, outs)):
-            xd = hx.to(dev, non_blocking=True)
-            dyd = hdy.to(dev, non_blocking=True)
-            h2d += hx.numel() * 2 + hdy.numel() * 2
-            y, ctx = qt.forward(xd, w_dev, out_dtype=torch.bfloat16, check_finite=False, bwd_xi=xi * 3 + i)
-            dx, dw = qt.backward(dyd, ctx, xi=xi * 3 + i, dx_dtype=torch.bfloat16, check_finite=False)
-            ox.copy_(dx, non_blocking=True)
-            ow.copy_(dw, non_blocking=True)
-            d2h += dx.numel() * 2 + dw.numel() * 4
-        return h2d, d2h
-    for i in range(2):
-        e2e_step(i)
-    torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for i in range(args.steps):
-        h2d, d2h = e2e_step(100 + i)
-    e.record()
-    torch.cuda.synchronize()
-    e2e_ms = s.elapsed_time(e) / args.steps
-    e2e = {"value": round(flops_per_step(T) / (e2e_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
-           "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-           "path": "paper_2505_14669_b200.forward/backward (C ABI), eager, pinned host x/dy in, dx/dw out"}
+    e2e = e2e_pipeline(qt, data, dev, args.steps)
 
     peaks = measured_peaks()
     fp4_peak = 4.0 * peaks["bf16_tflops"]
