@@ -194,7 +194,7 @@ def johnson_order(a, b):
     return first + rest
 
 
-def e2e_pipeline(qt, data, dev, steps):
+def e2e_pipeline(qt, data, dev, steps, outs_sink=None):
     """End to end through the public API with host buffers: every step uploads each shape's x and dy
     from pinned host memory and downloads its dx (bf16) and dw (fp32).  Three streams -- uploads,
     compute, downloads -- so PCIe runs both directions at once (full duplex, measured 92 GB/s
@@ -252,6 +252,8 @@ def e2e_pipeline(qt, data, dev, steps):
     e.record(comp)
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / steps
+    if outs_sink is not None:      # tests: the host results of the last step (xi = 100 + steps - 1)
+        outs_sink.extend(outs)
     return {"value": round(flops_per_step(data[0][0].shape[0]) / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
             "ms_per_step": round(ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "path": "paper_2505_14669_b200.forward/backward (C ABI), eager; pinned host x/dy in, dx/dw out; "
