@@ -194,7 +194,7 @@ def johnson_order(a, b):
     return first + rest
 
 
-def e2e_pipeline(qt, data, dev, steps, outs_sink=None):
+def e2e_pipeline(qt, data, dev, steps, outs_sink=None, world=1, rank=0):
     """End to end through the public API with host buffers: every step uploads each shape's x and dy
     from pinned host memory and downloads its dx (bf16) and dw (fp32).  Three streams -- uploads,
     compute, downloads -- so PCIe runs both directions at once (full duplex, measured 92 GB/s
@@ -203,7 +203,9 @@ def e2e_pipeline(qt, data, dev, steps, outs_sink=None):
     Device input buffers are double-buffered by step parity; shapes run in Johnson order
     (upload-light / download-heavy first), which minimises the two-stage makespan."""
     import torch
+    import torch.distributed as dist
 
+    T = data[0][0].shape[0]
     host = [(x.cpu().pin_memory(), dy.cpu().pin_memory()) for (x, _, dy) in data]
     outs = [(torch.empty(x.shape, dtype=torch.bfloat16).pin_memory(),
              torch.empty(w.shape, dtype=torch.float32).pin_memory()) for (x, w, _) in data]
@@ -227,8 +229,13 @@ def e2e_pipeline(qt, data, dev, steps, outs_sink=None):
                 ready = torch.cuda.Event()
                 ready.record(up)
             comp.wait_event(ready)
-            y, ctx = qt.forward(bx, data[i][1], out_dtype=torch.bfloat16, check_finite=False, bwd_xi=xi * 3 + i)
-            dx, dw = qt.backward(bdy, ctx, xi=xi * 3 + i, dx_dtype=torch.bfloat16, check_finite=False)
+            kw = dict(token_offset=rank * T, total_tokens=world * T) if world > 1 else {}
+            y, ctx = qt.forward(bx, data[i][1], out_dtype=torch.bfloat16, check_finite=False, bwd_xi=xi * 3 + i, **kw)
+            dx, dw = qt.backward(bdy, ctx, xi=xi * 3 + i, dx_dtype=torch.bfloat16, check_finite=False, **kw)
+            if world > 1:   # the data-parallel exchange of the step: bf16 all-reduce of dW before it goes down
+                buf = dw.to(torch.bfloat16)
+                dist.all_reduce(buf, async_op=True).wait()
+                dw.copy_(buf)
             done = torch.cuda.Event()
             done.record(comp)
             freed[par][i] = done
@@ -252,12 +259,17 @@ def e2e_pipeline(qt, data, dev, steps, outs_sink=None):
     e.record(comp)
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
     if outs_sink is not None:      # tests: the host results of the last step (xi = 100 + steps - 1)
         outs_sink.extend(outs)
-    return {"value": round(flops_per_step(data[0][0].shape[0]) / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+    return {"value": round(world * flops_per_step(T) / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
             "ms_per_step": round(ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "path": "paper_2505_14669_b200.forward/backward (C ABI), eager; pinned host x/dy in, dx/dw out; "
-                    "upload / compute / download streams (PCIe full duplex), double-buffered inputs"}
+                    "upload / compute / download streams (PCIe full duplex), double-buffered inputs; "
+                    + ("bytes per rank, dW all-reduced (bf16) before download" if world > 1 else "one GPU")}
 
 
 def run_ours(args, rank, world, local_rank):
@@ -341,6 +353,10 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    # end to end at N GPUs: every rank streams its own shard through its own PCIe link; max over ranks
+    if world > 1:
+        dist.barrier()
+    e2e = e2e_pipeline(qt, data, dev, args.steps, world=world, rank=rank)
     if rank != 0:
         return None
     table = kernel_table(qt, data, dev, reps=10)
@@ -364,7 +380,6 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     bf16_ms = s.elapsed_time(e) / args.steps
 
-    e2e = e2e_pipeline(qt, data, dev, args.steps)
 
     peaks = measured_peaks()
     fp4_peak = 4.0 * peaks["bf16_tflops"]
