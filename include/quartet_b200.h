@@ -65,6 +65,9 @@ extern "C" {
 #define QT_EPI_STORE 0             /* D = A B^T */
 #define QT_EPI_MASK_H 1            /* D = H32(A B^T (.) mask) * scale (qlinear.py:229-230, 249-250) */
 #define QT_EPI_MASK 2              /* D = (A B^T (.) mask) * scale (hadamard=False layers) */
+#define QT_EPI_ACCUMULATE 0x10     /* flag OR'ed into any epilogue: D += E, E first rounded to D's dtype (the sum
+                                      of several layers' dx in one buffer, as out.add_(tmp); 2-CTA kernel: TMA
+                                      reduce-add into L2) */
 #define QT_OUT_F32 0
 #define QT_OUT_BF16 1
 

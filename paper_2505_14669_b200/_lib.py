@@ -15,6 +15,7 @@ QT_IN_BF16, QT_IN_F32, QT_IN_MXFP4 = 0, 1, 2
 QT_TRANSFORM_NONE, QT_TRANSFORM_HADAMARD, QT_TRANSFORM_RANDOMIZED = 0, 1, 2
 QT_ROUND_QUEST, QT_ROUND_RTN, QT_ROUND_SR = 0, 1, 2
 QT_EPI_STORE, QT_EPI_MASK_H, QT_EPI_MASK = 0, 1, 2
+QT_EPI_ACCUMULATE = 0x10
 QT_OUT_F32, QT_OUT_BF16 = 0, 1
 QT_ERR_SHAPE, QT_ERR_ALIGN, QT_ERR_ARG, QT_ERR_TMA = 2001, 2002, 2003, 2004
 

@@ -214,12 +214,14 @@ int qt_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b_c
                  int64_t N, int64_t K, void* out, int out_dtype, int64_t ldo, int epilogue, const uint32_t* mask,
                  float scale, void* stream) {
     if (K % 32 != 0 || K <= 0 || N % 32 != 0 || M < 0) return QT_ERR_SHAPE;
+    const int accumulate = (epilogue & QT_EPI_ACCUMULATE) ? 1 : 0;
+    epilogue &= ~QT_EPI_ACCUMULATE;
     if (epilogue < QT_EPI_STORE || epilogue > QT_EPI_MASK) return QT_ERR_ARG;
     if (out_dtype != QT_OUT_F32 && out_dtype != QT_OUT_BF16) return QT_ERR_ARG;
     if (epilogue != QT_EPI_STORE && !mask) return QT_ERR_ARG;
     int esz = out_dtype == QT_OUT_BF16 ? 2 : 4;
     if (!al16(a_codes) || !al16(b_codes) || !al16(out) || (ldo * esz) % 16) return QT_ERR_ALIGN;
-    EpiParams ep{out, ldo, out_dtype == QT_OUT_BF16, epilogue, mask, N / 32, scale, g_gemm_dbg};
+    EpiParams ep{out, ldo, out_dtype == QT_OUT_BF16, epilogue, mask, N / 32, scale, g_gemm_dbg, accumulate};
     int rc = launch_gemm(a_codes, qt_codes_ld(K), a_sf, qt_sf_katoms(K), b_codes, qt_codes_ld(K), b_sf,
                          qt_sf_katoms(K), M, N, K, ep, (cudaStream_t)stream);
     return rc == 1001 || rc == 1002 ? QT_ERR_TMA : rc;

@@ -91,11 +91,18 @@ __device__ __forceinline__ void epi_store(const uint32_t (&acc)[CW / 32][32], in
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     uint32_t w[4];
+                    uint4 old = ep.accumulate ? o[q] : make_uint4(0, 0, 0, 0);
+                    const uint32_t* ow = reinterpret_cast<const uint32_t*>(&old);
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
                         const int i = q * 8 + 2 * t;
                         __nv_bfloat162 b2 = h ? __floats2bfloat162_rn(g.p[i].y, g.p[i + 1].y)
                                               : __floats2bfloat162_rn(g.p[i].x, g.p[i + 1].x);
+                        if (ep.accumulate) {  // bf16(old + bf16(new)), as out.add_(tmp) in bf16
+                            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ow[t]));
+                            const float2 b = __bfloat1622float2(b2);
+                            b2 = __floats2bfloat162_rn(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y));
+                        }
                         w[t] = *reinterpret_cast<uint32_t*>(&b2);
                     }
                     o[q] = make_uint4(w[0], w[1], w[2], w[3]);
@@ -105,8 +112,14 @@ __device__ __forceinline__ void epi_store(const uint32_t (&acc)[CW / 32][32], in
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     const int i = 4 * q;
-                    o[q] = h ? make_float4(g.p[i].y, g.p[i + 1].y, g.p[i + 2].y, g.p[i + 3].y)
-                             : make_float4(g.p[i].x, g.p[i + 1].x, g.p[i + 2].x, g.p[i + 3].x);
+                    float4 v = h ? make_float4(g.p[i].y, g.p[i + 1].y, g.p[i + 2].y, g.p[i + 3].y)
+                                 : make_float4(g.p[i].x, g.p[i + 1].x, g.p[i + 2].x, g.p[i + 3].x);
+                    if (ep.accumulate) {
+                        const float4 a = o[q];
+                        v = make_float4(__fadd_rn(a.x, v.x), __fadd_rn(a.y, v.y), __fadd_rn(a.z, v.z),
+                                        __fadd_rn(a.w, v.w));
+                    }
+                    o[q] = v;
                 }
             }
         }
@@ -325,6 +338,12 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
                  "r"(smem_u32(src)), "r"(x), "r"(y)
                  : "memory");
 }
+// element-wise out += box through the TMA unit (reduction in L2, one rounding to the map's dtype)
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int x, int y) {
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(x), "r"(y)
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -387,7 +406,10 @@ __device__ __forceinline__ void epi_stage(const uint32_t (&acc)[CW / 32][32], in
                 fence_proxy_async_cta();
                 named_bar(1 + half, 128);
                 if (issuer) {
-                    tma_store_2d(tmO, box, ep.out_bf16 ? col0 : col0 + 32 * h, y0);
+                    if (ep.accumulate)
+                        tma_reduce_add_2d(tmO, box, ep.out_bf16 ? col0 : col0 + 32 * h, y0);
+                    else
+                        tma_store_2d(tmO, box, ep.out_bf16 ? col0 : col0 + 32 * h, y0);
                     bulk_commit();
                 }
             }

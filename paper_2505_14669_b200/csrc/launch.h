@@ -45,6 +45,7 @@ struct EpiParams {
     int64_t ldm;             // words per mask row
     float scale;
     int dbg;                 // experiment knobs (0 in production)
+    int accumulate;          // D += epilogue result (rounded to D's dtype first), QT_EPI_ACCUMULATE
 };
 
 int launch_transform_rows(const float* x, float* out, int64_t rows, int64_t cols, int transform,

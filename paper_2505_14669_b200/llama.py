@@ -390,7 +390,7 @@ class Trainer:
             gr["lr"] = lr
         logits = self.model(tokens)
         loss = cross_entropy(logits.view(-1, logits.shape[-1]), targets.reshape(-1))
-        self.opt.zero_grad(set_to_none=False)
+        self.opt.zero_grad(set_to_none=True)   # backward assigns each gradient (no fill, no accumulate pass)
         loss.backward()                # bucket all-reduces start inside backward (hooks)
         self.bucket.finish()
         torch.nn.utils.clip_grad_norm_(self.bucket.params, self.grad_clip)

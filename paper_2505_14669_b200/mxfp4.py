@@ -241,16 +241,22 @@ def quant_dual(x: torch.Tensor, rounding: int, *, transform: int, signs: torch.T
 
 
 def gemm(a: MXOperand, b: MXOperand, *, out_dtype=torch.float32, mask: torch.Tensor | None = None,
-         hadamard: bool = True, scale: float = 1.0, out: torch.Tensor | None = None) -> torch.Tensor:
+         hadamard: bool = True, scale: float = 1.0, out: torch.Tensor | None = None,
+         accumulate: bool = False) -> torch.Tensor:
     """deq(a) @ deq(b).T on tcgen05 (gemm_lp, qlinear.py:96-111); with `mask`, the fused
-    H32(D * mask) * scale epilogue (qlinear.py:229-230)."""
+    H32(D * mask) * scale epilogue (qlinear.py:229-230).  accumulate=True adds the result (rounded to
+    out's dtype) into `out` instead of overwriting it, bit-identical to out.add_(gemm(...))."""
     if a.cols != b.cols:
         raise ValueError(f"contraction mismatch: {a.cols} vs {b.cols}")
     M, N, K = a.rows, b.rows, a.cols
+    if accumulate and (out is None or tuple(out.shape) != (M, N)):
+        raise ValueError("accumulate=True needs an [M, N] out tensor")
     if out is None:
         out = torch.empty((M, N), dtype=out_dtype, device=a.codes.device)
     odt = _lib.QT_OUT_BF16 if out.dtype == torch.bfloat16 else _lib.QT_OUT_F32
     epi = _lib.QT_EPI_STORE if mask is None else (_lib.QT_EPI_MASK_H if hadamard else _lib.QT_EPI_MASK)
+    if accumulate:
+        epi |= _lib.QT_EPI_ACCUMULATE
     rc = _lib.load().qt_gemm_mxf4(a.codes.data_ptr(), a.sf.data_ptr(), b.codes.data_ptr(), b.sf.data_ptr(),
                                   M, N, K, out.data_ptr(), odt, out.stride(0), epi,
                                   mask.data_ptr() if mask is not None else None, float(scale),

@@ -95,10 +95,12 @@ class QuartetLinearGroupFn(torch.autograd.Function):
             dy2 = dy.reshape(-1, dy.shape[-1])
             if dy2.dtype not in (torch.bfloat16, torch.float32):
                 dy2 = dy2.float()
-            dx, dw = qlinear.backward(dy2.contiguous(), lctx, xi, ctx.rounding, dx_dtype=dx_dtype,
-                                      dw_dtype=torch.float32, check_finite=False, token_offset=ShardContext.offset,
-                                      total_tokens=ShardContext.total)
-            dx_sum = dx if dx_sum is None else dx_sum.add_(dx)  # in x's dtype, as autograd would accumulate
+            # the layers' dx are summed in x's dtype (as autograd would accumulate them) by the dx GEMM's
+            # epilogue adding into the first layer's dx (QT_EPI_ACCUMULATE): no separate add pass
+            dx_sum, dw = qlinear.backward(dy2.contiguous(), lctx, xi, ctx.rounding, dx_dtype=dx_dtype,
+                                          dw_dtype=torch.float32, check_finite=False,
+                                          token_offset=ShardContext.offset, total_tokens=ShardContext.total,
+                                          dx_accumulate=dx_sum)
             dws.append(dw.to(wdt))
         ctx.lctxs = None
         return (dx_sum.reshape(ctx.x_shape), None, None, None, None, *dws)

@@ -244,8 +244,12 @@ def _rounding_code(rounding: str) -> int:
 def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn",
              dx_dtype: torch.dtype = torch.float32, dw_dtype: torch.dtype = torch.float32,
              check_finite: bool = True, return_operands: bool = False, token_offset: int = 0,
-             total_tokens: int | None = None):
+             total_tokens: int | None = None, dx_accumulate: torch.Tensor | None = None):
     """Input and weight gradients from the saved context and upstream dy (qlinear.py:178-252).
+
+    dx_accumulate: an existing [batch, d_in] gradient buffer that this layer's dx is added into by the
+    GEMM epilogue (several layers reading the same x, nn.QuartetLinearGroupFn); the returned dx is that
+    buffer, bit-identical to dx_accumulate.add_(dx).
 
     Data-parallel shards: a rank holding tokens [token_offset, token_offset + batch) of a global batch of
     `total_tokens` passes both; its randomized-Hadamard signs and stochastic-rounding stream positions
@@ -291,7 +295,8 @@ def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn"
     wt_q = ea.wt_q if ea is not None else quant_cols(ctx.w_q, rc, transform=transform, signs=d_signs,
                                                      prescale=PRE_SCALE,
                                                      sr_seed=derive_seed(xi, _TAG_BWD_W) if sr else 0, err=err)
-    dx = gemm(g_q, wt_q, out_dtype=dx_dtype, mask=ctx.x_q.mask, hadamard=ctx.hadamard, scale=_POST_F32)
+    dx = gemm(g_q, wt_q, out_dtype=dx_dtype, mask=ctx.x_q.mask, hadamard=ctx.hadamard, scale=_POST_F32,
+              out=dx_accumulate, accumulate=dx_accumulate is not None)
 
     # weight gradient: contract over batch (qlinear.py:232-250)
     xt_q = ea.xt_q if ea is not None else quant_cols(ctx.x_q, rc, transform=transform, signs=t_signs,

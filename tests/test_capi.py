@@ -59,6 +59,8 @@ def test_argument_errors_without_gpu(lib):
                              None) == 2001
     assert lib.qt_gemm_mxf4(None, None, None, None, 32, 32, 48, None, 0, 32, 0, None, 1.0, None) == 2001
     assert lib.qt_gemm_mxf4(None, None, None, None, 32, 32, 64, None, 7, 32, 0, None, 1.0, None) == 2003
+    assert lib.qt_gemm_mxf4(None, None, None, None, 32, 32, 64, None, 0, 32, 0x13, None, 1.0, None) == 2003  # ACCUMULATE | 3
+    assert lib.qt_gemm_mxf4(None, None, None, None, 32, 32, 64, None, 0, 32, 0x11, None, 1.0, None) == 2003  # mask missing
 
 
 def test_glue_entry_points_reject_bad_shapes(lib):

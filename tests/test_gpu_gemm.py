@@ -149,3 +149,24 @@ def test_gemm_cluster8_multicast_kernel(qt, oracle, mnk):
         test_gemm_random(qt, oracle, mnk)
     finally:
         L.qt_debug_set_gemm(0)
+
+
+@pytest.mark.parametrize("mn", [(512, 768), (288, 512), (256, 96), (640, 1184)])
+@pytest.mark.parametrize("odt", [torch.bfloat16, torch.float32])
+def test_gemm_accumulate_equals_add(qt, mn, odt):
+    """QT_EPI_ACCUMULATE: the epilogue adds its (dtype-rounded) result into out -- TMA reduce-add on the
+    2-CTA kernel (N % 256 == 0), read-add-write on the 1-CTA kernel -- bit-identical to out.add_(gemm)."""
+    M, N = mn
+    K = 256
+    g = torch.Generator(device="cuda").manual_seed(M * N)
+    from paper_2505_14669_b200 import _lib
+
+    A = qt.quant_rows(torch.randn(M, K, device="cuda", generator=g), _lib.QT_TRANSFORM_NONE, _lib.QT_ROUND_RTN)
+    B = qt.quant_rows(torch.randn(N, K, device="cuda", generator=g), _lib.QT_TRANSFORM_NONE, _lib.QT_ROUND_RTN)
+    mask = torch.randint(-2**31, 2**31 - 1, (M, N // 32), device="cuda", dtype=torch.int32, generator=g)
+    base = (torch.randn(M, N, device="cuda", generator=g) * 3).to(odt)
+    for kw in ({}, {"mask": mask, "hadamard": True, "scale": 16 / 9}):
+        want = base.clone().add_(qt.gemm(A, B, out_dtype=odt, **kw))
+        got = base.clone()
+        qt.gemm(A, B, out=got, accumulate=True, **kw)
+        assert torch.equal(got, want), (mn, odt, kw)

@@ -16,4 +16,4 @@ from torch.profiler import profile, ProfilerActivity
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as p:
     tr.step(tok, tgt)
     torch.cuda.synchronize()
-print(p.key_averages().table(sort_by="cuda_time_total", row_limit=30, max_name_column_width=70))
+print(p.key_averages().table(sort_by="cuda_time_total", row_limit=40, max_name_column_width=160))
