@@ -360,7 +360,7 @@ __device__ __forceinline__ void epi_stage(const uint32_t (&acc)[CW / 32][32], in
 #pragma unroll
         for (int i = 0; i < 32; ++i)
             g.p[i] = make_float2(__uint_as_float(acc[2 * pj][i]), __uint_as_float(acc[2 * pj + 1][i]));
-        if (ep.mode != kEpiStore) {
+        if (ep.mode != kEpiStore && !(ep.dbg & 0x400)) {   // dbg 0x400 (timing only): no mask / FWHT / scale
             const uint32_t mA = live ? __ldg(ep.mask + (int64_t)row * ep.ldm + col0 / 32) : 0u;
             const uint32_t mB = live ? __ldg(ep.mask + (int64_t)row * ep.ldm + col0 / 32 + 1) : 0u;
 #pragma unroll
@@ -405,7 +405,7 @@ __device__ __forceinline__ void epi_stage(const uint32_t (&acc)[CW / 32][32], in
             if (ep.out_bf16 ? (h == 1) : true) {
                 fence_proxy_async_cta();
                 named_bar(1 + half, 128);
-                if (issuer) {
+                if (issuer && !(ep.dbg & 0x200)) {   // dbg 0x200 (timing only): no TMA stores
                     if (ep.accumulate)
                         tma_reduce_add_2d(tmO, box, ep.out_bf16 ? col0 : col0 + 32 * h, y0);
                     else
