@@ -473,7 +473,11 @@ __global__ void __launch_bounds__(256, 2) k_quant(TileArgs a) {
                 a.col_out.sf[sf_offset(orow + 1, ogrp, a.col_out.katoms)] = (uint8_t)eB;
             }
         }
-        __syncthreads();
+        // Before the next iteration refills this stage buffer (cp.async at its top) and rewrites the LUTs, every
+        // thread must be done with this tile.  The fused forward (codes-sourced col pass from a dense tile) needs
+        // no barrier here: its col pass reads only codes_s / T, which the next tile rewrites after the barrier
+        // that follows cp_async_wait1, and the row pass that read the stage and rlut ended at the mid barrier.
+        if (!(COL == kColCodes && IN != kInMXFP4)) __syncthreads();
     }
 }
 
