@@ -113,6 +113,9 @@ def gemm_nt(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     a32, b32 = _to_f32_exact(a), _to_f32_exact(b)
     if a32.shape[1] != b32.shape[1]:
         raise ValueError(f"contraction mismatch: {a32.shape[1]} vs {b32.shape[1]}")
+    np_out = np.float64 if a.dtype == np.float64 else np.float32
+    if a32.size == 0 or b32.size == 0:  # empty rows, columns or contraction: the reference returns zeros
+        return np.zeros((a32.shape[0], b32.shape[0]), np_out)
     ad, m, k = _pad(a32)
     n = b32.shape[0]
     if n % GROUP:  # the GEMM epilogue works on 32-column chunks: pad B with zero rows
@@ -122,7 +125,6 @@ def gemm_nt(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     B = quant_rows(bd, _lib.QT_TRANSFORM_NONE, _lib.QT_ROUND_RTN)
     if not (torch.equal(A.dequantize(torch.float32), ad) and torch.equal(B.dequantize(torch.float32), bd)):
         raise ValueError("b200 backend gemm_nt: operands are not MXFP4 grids (dequantize-then-matmul inputs)")
-    np_out = np.float64 if a.dtype == np.float64 else np.float32
     return gemm(A, B, out_dtype=torch.float32)[:, :n].cpu().numpy().astype(np_out)
 
 

@@ -75,3 +75,19 @@ def test_gemm_nt_on_mxfp4_operands(kb, oracle):
 def test_rejects_non_fp32_inputs(kb):
     with pytest.raises(ValueError):
         kb.quantize_rtn(np.array([[0.1] * 32]), 32)
+
+
+@pytest.mark.parametrize("shape", [(0, 64), (3, 0), (0, 0)])
+def test_empty_inputs_match_reference(kb, oracle, shape):
+    """Empty rows / columns: the reference's kernels return empty (or, for gemm_nt with an empty
+    contraction, all-zero) arrays of the right shapes and dtypes without touching a kernel."""
+    x = np.zeros(shape, np.float32)
+    for got, want in ((kb.quantize_rtn(x.astype(np.float64), 32), oracle.quantize_rtn(x, 32)),
+                      (kb.quantize_sr(x.astype(np.float64), 32, 5, 0), oracle.quantize_sr(x, 32, 5, 0)),
+                      (kb.quantize_quest(x.astype(np.float64), 32, 1 / 16), oracle.quantize_quest(x, 32, 1 / 16))):
+        for g, w in zip(got, want):
+            assert g.shape == w.shape and g.dtype == w.dtype
+    assert kb.fwht(x, 32).shape == shape
+    b = np.zeros((2, shape[1]), np.float32)
+    g, w = kb.gemm_nt(x, b), oracle.gemm_nt(x, b)
+    assert g.shape == w.shape and np.array_equal(g, w)
