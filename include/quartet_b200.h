@@ -46,6 +46,10 @@ extern "C" {
 
 #define QT_ABI_VERSION 1
 
+/* Empty dimensions (rows, cols or a GEMM's M / N = 0; the reference accepts batch = 0) are valid: after the
+ * shape and enum checks the call returns 0 without reading any pointer.  A GEMM with K = 0 writes zeros
+ * (every epilogue of a zero product is zero) or, with QT_EPI_ACCUMULATE, leaves D unchanged. */
+
 /* error codes beyond cudaError_t */
 #define QT_ERR_SHAPE 2001  /* axis not a multiple of 32 / mismatched operands (ValueError upstream) */
 #define QT_ERR_ALIGN 2002  /* pointer or leading dimension not 16-byte aligned */

@@ -73,7 +73,9 @@ int qt_sign_bits_pair(uint32_t* a, int64_t start_a, int64_t n_a, uint32_t* b, in
 int qt_fwht32(const float* x, float* out, int64_t rows, int64_t cols, int transform, const uint32_t* sign_bits,
              float prescale, void* stream) {
     if (cols % 32 != 0 || rows < 0) return QT_ERR_SHAPE;
-    if (transform < 0 || transform > 2 || (transform == QT_TRANSFORM_RANDOMIZED && !sign_bits)) return QT_ERR_ARG;
+    if (transform < 0 || transform > 2) return QT_ERR_ARG;
+    if (rows == 0 || cols == 0) return 0;  // nothing to quantize: no pointer is read (empty sign vectors are null)
+    if (transform == QT_TRANSFORM_RANDOMIZED && !sign_bits) return QT_ERR_ARG;
     return launch_transform_rows(x, out, rows, cols, transform, sign_bits, prescale, (cudaStream_t)stream);
 }
 
@@ -84,6 +86,7 @@ int qt_quant_rows(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_
     if (cols % 32 != 0 || rows < 0) return QT_ERR_SHAPE;
     if (in_dtype != QT_IN_BF16 && in_dtype != QT_IN_F32) return QT_ERR_ARG;
     if (rounding < 0 || rounding > 2 || transform < 0 || transform > 2) return QT_ERR_ARG;
+    if (rows == 0 || cols == 0) return 0;  // nothing to quantize: no pointer is read (empty sign vectors are null)
     if (transform == QT_TRANSFORM_RANDOMIZED && !sign_bits) return QT_ERR_ARG;
     int esz = in_dtype == QT_IN_BF16 ? 2 : 4;
     if (!al16(x) || (ldx * esz) % 16 || !al16(codes) || ldc % 16) return QT_ERR_ALIGN;
@@ -97,9 +100,10 @@ int qt_quant_cols(const void* x, int in_dtype, int64_t ldx, const uint8_t* mx_co
                   const uint32_t* sign_bits, float prescale, int rounding, uint64_t sr_seed, uint64_t counter_start,
                   int64_t counter_ld, uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, int* err,
                   void* stream) {
-    if (rows % 32 != 0 || cols % 32 != 0) return QT_ERR_SHAPE;
+    if (rows % 32 != 0 || cols % 32 != 0 || rows < 0 || cols < 0) return QT_ERR_SHAPE;
     if (in_dtype < 0 || in_dtype > 2 || rounding < 0 || rounding > 2 || transform < 0 || transform > 2)
         return QT_ERR_ARG;
+    if (rows == 0 || cols == 0) return 0;  // nothing to quantize: no pointer is read (empty sign vectors are null)
     if (transform == QT_TRANSFORM_RANDOMIZED && !sign_bits) return QT_ERR_ARG;
     if (in_dtype == QT_IN_MXFP4) {
         if (!al16(mx_codes) || mx_ldc % 16) return QT_ERR_ALIGN;
@@ -120,10 +124,11 @@ int qt_quant_dual(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_
                   int64_t col_counter_ld, uint8_t* row_codes, int64_t row_ldc, uint8_t* row_sf, int64_t row_katoms,
                   uint32_t* row_mask, uint8_t* col_codes, int64_t col_ldc, uint8_t* col_sf, int64_t col_katoms,
                   int* err, void* stream) {
-    if (rows % 32 != 0 || cols % 32 != 0) return QT_ERR_SHAPE;
+    if (rows % 32 != 0 || cols % 32 != 0 || rows < 0 || cols < 0) return QT_ERR_SHAPE;
     if ((in_dtype != QT_IN_BF16 && in_dtype != QT_IN_F32) || rounding < 0 || rounding > 2 || transform < 0 ||
         transform > 2)
         return QT_ERR_ARG;
+    if (rows == 0 || cols == 0) return 0;  // nothing to quantize: no pointer is read (empty sign vectors are null)
     if (transform == QT_TRANSFORM_RANDOMIZED && (!row_sign_bits || !col_sign_bits)) return QT_ERR_ARG;
     int esz = in_dtype == QT_IN_BF16 ? 2 : 4;
     if (!al16(x) || (ldx * esz) % 16 || !al16(row_codes) || row_ldc % 16 || !al16(col_codes) || col_ldc % 16)
@@ -151,10 +156,11 @@ int qt_quant_fused(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64
                    const uint32_t* col_sign_bits, float col_prescale, int col_rounding, uint64_t col_seed,
                    uint64_t col_counter_start, int64_t col_counter_ld, uint8_t* col_codes, int64_t col_ldc,
                    uint8_t* col_sf, int64_t col_katoms, int* err, int* fallbacks, void* stream) {
-    if (rows % 32 != 0 || cols % 32 != 0 || rows < 0) return QT_ERR_SHAPE;
+    if (rows % 32 != 0 || cols % 32 != 0 || rows < 0 || cols < 0) return QT_ERR_SHAPE;
     if (in_dtype != QT_IN_BF16 && in_dtype != QT_IN_F32) return QT_ERR_ARG;
     if (row_rounding < 0 || row_rounding > 2 || col_rounding < 1 || col_rounding > 2) return QT_ERR_ARG;
     if (row_transform < 0 || row_transform > 2 || col_transform < 0 || col_transform > 2) return QT_ERR_ARG;
+    if (rows == 0 || cols == 0) return 0;  // nothing to quantize: no pointer is read (empty sign vectors are null)
     if ((row_transform == QT_TRANSFORM_RANDOMIZED && !row_sign_bits) ||
         (col_transform == QT_TRANSFORM_RANDOMIZED && !col_sign_bits))
         return QT_ERR_ARG;
@@ -213,13 +219,19 @@ int qt_requant_t(const uint8_t* codes, const uint8_t* sf, int64_t rows, int64_t 
 int qt_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_sf, const uint8_t* b_codes, const uint8_t* b_sf, int64_t M,
                  int64_t N, int64_t K, void* out, int out_dtype, int64_t ldo, int epilogue, const uint32_t* mask,
                  float scale, void* stream) {
-    if (K % 32 != 0 || K <= 0 || N % 32 != 0 || M < 0) return QT_ERR_SHAPE;
+    if (K % 32 != 0 || K < 0 || N % 32 != 0 || N < 0 || M < 0) return QT_ERR_SHAPE;
     const int accumulate = (epilogue & QT_EPI_ACCUMULATE) ? 1 : 0;
     epilogue &= ~QT_EPI_ACCUMULATE;
     if (epilogue < QT_EPI_STORE || epilogue > QT_EPI_MASK) return QT_ERR_ARG;
     if (out_dtype != QT_OUT_F32 && out_dtype != QT_OUT_BF16) return QT_ERR_ARG;
-    if (epilogue != QT_EPI_STORE && !mask) return QT_ERR_ARG;
+    if (M == 0 || N == 0) return 0;
     int esz = out_dtype == QT_OUT_BF16 ? 2 : 4;
+    if (K == 0) {  // empty contraction: every epilogue of a zero product is zero (D += 0 leaves D as it is)
+        if (accumulate) return 0;
+        if ((ldo < N) || !out) return QT_ERR_ARG;
+        return (int)cudaMemset2DAsync(out, (size_t)(ldo * esz), 0, (size_t)(N * esz), (size_t)M, (cudaStream_t)stream);
+    }
+    if (epilogue != QT_EPI_STORE && !mask) return QT_ERR_ARG;
     if (!al16(a_codes) || !al16(b_codes) || !al16(out) || (ldo * esz) % 16) return QT_ERR_ALIGN;
     EpiParams ep{out, ldo, out_dtype == QT_OUT_BF16, epilogue, mask, N / 32, scale, g_gemm_dbg, accumulate};
     int rc = launch_gemm(a_codes, qt_codes_ld(K), a_sf, qt_sf_katoms(K), b_codes, qt_codes_ld(K), b_sf,

@@ -71,3 +71,14 @@ def test_glue_entry_points_reject_bad_shapes(lib):
     assert lib.qt_rmsnorm(None, None, None, None, None, None, 8, 100, 1e-6, 0, None) == 2001  # d % 256
     assert lib.qt_rmsnorm(None, None, None, None, None, None, 8, 10240, 1e-6, 0, None) == 2001
     assert lib.qt_cross_entropy(None, None, 8, 7, None, None, None, None, 1.0, 0, None) == 2001
+
+
+def test_empty_dimensions_are_no_ops(lib):
+    """An empty row / column / token dimension is valid (the reference accepts batch = 0): the entry points
+    return 0 before reading any pointer -- the sign vector of an empty dimension is legitimately null."""
+    assert lib.qt_quant_rows(None, 0, 32, 0, 32, 2, None, 1.0, 0, 0, 0, 0, None, 16, None, 2, None, None, None,
+                             None) == 0
+    assert lib.qt_fwht32(None, None, 0, 64, 2, None, 1.0, None) == 0
+    assert lib.qt_gemm_mxf4(None, None, None, None, 0, 32, 64, None, 0, 32, 1, None, 1.0, None) == 0   # M = 0
+    assert lib.qt_gemm_mxf4(None, None, None, None, 32, 32, 0, None, 0, 32, 0x11, None, 1.0, None) == 0  # D += 0
+    assert lib.qt_gemm_mxf4(None, None, None, None, -32, 32, 64, None, 0, 32, 0, None, 1.0, None) == 2001

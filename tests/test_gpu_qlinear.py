@@ -107,6 +107,16 @@ def test_shape_validation(qt):
         qt.forward(torch.ones(32, 32, device=dev), torch.ones(32, 32, device=dev), scheme=qt.SR_ABSMAX)
 
 
+@pytest.mark.parametrize("bwd_xi", [None, 3])
+def test_empty_batch(qt, bwd_xi):
+    """batch = 0 passes the reference's checks (0 % 32 == 0): y and dx are empty, dW is all zeros."""
+    x, w = torch.zeros(0, 64, device="cuda"), torch.randn(32, 64, device="cuda")
+    y, ctx = qt.forward(x, w, bwd_xi=bwd_xi)
+    assert tuple(y.shape) == (0, 32)
+    dx, dw = qt.backward(torch.zeros(0, 32, device="cuda"), ctx, xi=3)
+    assert tuple(dx.shape) == (0, 64) and tuple(dw.shape) == (32, 64) and torch.all(dw == 0)
+
+
 def test_zero_dy_gives_zero_grads(qt):
     x = torch.randn(64, 64, device="cuda")
     w = torch.randn(32, 64, device="cuda")
