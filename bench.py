@@ -11,8 +11,8 @@ for x / dy at T=16384), so no L2 flush is needed between steps.
 Multi-GPU (torchrun): data-parallel, weak scaling; each rank runs its own T tokens and the dW of
 every shape is all-reduced in bf16 over NCCL (the only exchange step in DP training).
 
---impl reference times the reference algorithm on the host CPU (oracle/ C restatement of
-mx4train's native kernels, all host threads) on a bounded token slice of the same workload.
+--impl reference times the reference itself (mx4train.qlinear from baseline/_ref, native backend) on the
+host CPU, one worker process per core, on bounded token slices of the same workload.
 """
 
 from __future__ import annotations
@@ -105,26 +105,60 @@ def ncu_traffic() -> dict:
     return {}
 
 
-def cpu_baseline_sample(threads: int, tokens: int = 256) -> dict:
-    """The reference algorithm on the host (oracle port), one fwd+bwd per shape on a token slice."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def import_reference():
+    """The unmodified reference (mx4train) as pip-installed into baseline/_ref, native (Cython) backend:
+    the CPU implementation of the path this bench's reference arm and cpu_baseline time.  Test/measurement
+    infrastructure only -- nothing on the GPU path imports it."""
+    if not os.path.isdir(os.path.join(REF_DIR, "mx4train")):
+        raise RuntimeError(f"reference not installed in {REF_DIR} (python -m pip install --no-index "
+                           "--no-build-isolation --no-deps --target baseline/_ref <copy of /root/reference/pkg>)")
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    os.environ["MX4TRAIN_BACKEND"] = "native"
+    from mx4train import qlinear
+    from mx4train._backend import BACKEND
+
+    if BACKEND != "native":
+        raise RuntimeError(f"reference backend is {BACKEND!r}, expected the compiled 'native' kernels")
+    return qlinear
+
+
+def _bf16_valued(a):
+    """Round an fp32 array to bf16-representable values (RNE), like the GPU arm's bf16 inputs."""
     import numpy as np
 
-    from oracle import oracle
+    b = a.astype(np.float32).view(np.uint32)
+    b = ((b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return b.view(np.float32)
 
-    oracle.build()
-    oracle.set_threads(threads)
-    r = np.random.default_rng(0)
+
+def ref_inputs(tokens: int, d_in: int, d_out: int, seed: int):
+    """Synthetic inputs of one shape (x, dy ~ N(0,1) bf16-valued; W ~ N(0, 1/d_in) fp32)."""
+    import numpy as np
+
+    r = np.random.default_rng(seed)
+    x = _bf16_valued(r.standard_normal((tokens, d_in), dtype=np.float32))
+    w = (r.standard_normal((d_out, d_in), dtype=np.float32) / np.float32(np.sqrt(d_in))).astype(np.float32)
+    dy = _bf16_valued(r.standard_normal((tokens, d_out), dtype=np.float32))
+    return x, w, dy
+
+
+def cpu_baseline_sample(tokens: int = 128) -> dict:
+    """cpu_baseline: the reference itself (mx4train.qlinear.forward + backward, native backend, one core --
+    its kernels are single-threaded) on a bounded sample of the bench workload: one fwd+bwd of each of the
+    three Llama-7B shapes on `tokens` tokens (of the 16384)."""
+    ql = import_reference()
     total_flop, total_s = 0.0, 0.0
-    for d_in, d_out in SHAPES:
-        x = r.standard_normal((tokens, d_in), dtype=np.float32)
-        w = (r.standard_normal((d_out, d_in), dtype=np.float32) / np.sqrt(d_in)).astype(np.float32)
-        dy = r.standard_normal((tokens, d_out), dtype=np.float32)
+    for i, (d_in, d_out) in enumerate(SHAPES):
+        x, w, dy = ref_inputs(tokens, d_in, d_out, seed=i)
         t0 = time.perf_counter()
-        _, ctx = oracle.forward(x, w)
-        oracle.backward(dy, ctx, xi=7)
+        _, ctx = ql.forward(x, w)
+        ql.backward(dy, ctx, 7)
         total_s += time.perf_counter() - t0
         total_flop += 6.0 * tokens * d_in * d_out
-    oracle.set_threads(1)
     return {"flop": total_flop, "seconds": total_s}
 
 
@@ -453,54 +487,86 @@ def run_train(rank, world, local_rank):
     return out
 
 
+_REF = {}   # inherited by the forked reference workers: module, inputs, start barrier
+
+
+def _ref_worker(job):
+    """One reference worker's share of a step: its own token slice through the unmodified
+    mx4train.qlinear.forward / backward (data-parallel decomposition: every worker re-quantizes W, as
+    every data-parallel rank must).  Returns (start, end) on the host's monotonic clock."""
+    shape, k, xi = job
+    ql = _REF["ql"]
+    x, w, dy = _REF["data"][shape]
+    T = _REF["tokens"]
+    xs, dys = x[k * T:(k + 1) * T], dy[k * T:(k + 1) * T]
+    _REF["barrier"].wait()
+    t0 = time.perf_counter()
+    _, ctx = ql.forward(xs, w)
+    ql.backward(dys, ctx, xi)
+    return t0, time.perf_counter()
+
+
 def run_reference(args, rank, world):
-    """Reference CPU implementation of the path (oracle port of mx4train's native kernels), all host
-    threads.  Each step is a bounded sample of the workload: one fwd+bwd of one of the three shapes
-    (cycling) on --ref-tokens tokens; value = sampled FLOP / sampled seconds."""
+    """Reference arm: the reference's own CPU implementation of the path -- mx4train.qlinear.forward +
+    backward (QuEST forward, RTN backward, hadamard=True; native Cython kernels) from baseline/_ref -- on the
+    host cores.  The reference's kernels are single-threaded, so it uses every core as one worker process
+    per core (bounded by host memory), each running its own --ref-tokens token slice of the same shape
+    (data parallel, W re-quantized per worker as per data-parallel rank).  A step = one fwd+bwd of one of
+    the three Llama-7B shapes (cycling) on every worker; value = FLOP of all workers / step wall time
+    (first start to last end), summed over the timed steps.  Under torchrun only rank 0 runs."""
     if rank != 0:
         return None
-    import numpy as np
+    import multiprocessing as mp
 
-    from oracle import oracle
+    ql = import_reference()
+    cores = os.cpu_count() or 1
+    try:
+        import psutil
 
-    oracle.build()
-    threads = os.cpu_count() or 1
-    oracle.set_threads(threads)
+        avail_gb = psutil.virtual_memory().available / 2**30
+    except Exception:
+        avail_gb = 64.0
+    # the 11008 x 4096 shapes hold a few f32 / f64 copies of W per worker (~2 GB transient)
+    P = max(1, min(cores, args.ref_workers or cores, int(avail_gb // 3)))
     T = args.ref_tokens
-    r = np.random.default_rng(0)
-    data = []
-    for d_in, d_out in SHAPES:
-        data.append((r.standard_normal((T, d_in), dtype=np.float32),
-                     (r.standard_normal((d_out, d_in), dtype=np.float32) / np.sqrt(d_in)).astype(np.float32),
-                     r.standard_normal((T, d_out), dtype=np.float32)))
-
-    def one(i):
-        x, w, dy = data[i % len(SHAPES)]
-        t0 = time.perf_counter()
-        _, ctx = oracle.forward(x, w)
-        oracle.backward(dy, ctx, xi=7 + i)
-        return 6.0 * T * x.shape[1] * w.shape[0], time.perf_counter() - t0
-
-    for i in range(min(args.warmup, 1)):
-        one(i)
+    _REF.update(ql=ql, tokens=T, data=[ref_inputs(P * T, d_in, d_out, seed=i) for i, (d_in, d_out) in
+                                       enumerate(SHAPES)])
+    ctx = mp.get_context("fork")
+    _REF["barrier"] = ctx.Barrier(P)
     flop = sec = 0.0
     done = 0
-    for i in range(args.steps):
-        f, t = one(i)
-        flop += f
-        sec += t
-        done += 1
-        if sec > 150.0:  # keep the whole reference arm within a few minutes on small hosts
-            break
+    budget = args.ref_budget_s
+    with ctx.Pool(P) as pool:
+        def one(i):
+            s = i % len(SHAPES)
+            ts = pool.map(_ref_worker, [(s, k, 7 + i) for k in range(P)], chunksize=1)
+            d_in, d_out = SHAPES[s]
+            return 6.0 * P * T * d_in * d_out, max(e for _, e in ts) - min(b for b, _ in ts)
+
+        t_all = time.perf_counter()
+        for i in range(min(args.warmup, 1)):
+            one(i)
+        for i in range(args.steps):
+            f, t = one(i)
+            flop += f
+            sec += t
+            done += 1
+            if time.perf_counter() - t_all > budget:  # keep the whole arm within a few minutes
+                break
     v = flop / sec / 1e12
     return {
         "impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "TFLOP/s", "n_gpus": world,
-        "steps": args.steps, "steps_timed": done, "warmup": args.warmup, "ms_per_step": round(1e3 * sec / done, 2),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (simulated MXFP4)",
-        "data": "synthetic", "config": {"workload": "QuartetLinear fwd+bwd, Llama-7B projection shapes",
-                                        "shapes_din_dout": SHAPES, "tokens_per_step": T},
-        "cpu_baseline": {"value": round(v, 6), "unit": "TFLOP/s", "cores": threads, "kind": "port",
-                         "sample": f"per step one fwd+bwd of one shape (cycling) on {T} tokens of the 16384"},
+        "steps": args.steps, "steps_timed": done, "warmup": min(args.warmup, 1), "ms_per_step": round(1e3 * sec / done, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 (fp32 work dtype; MXFP4 simulated in f64 quantizers, as the reference)",
+        "data": "synthetic (x, dy ~ N(0,1) bf16-valued; W ~ N(0,1/d_in) fp32)",
+        "config": {"workload": "QuartetLinear fwd+bwd, Llama-7B projection shapes (BASELINE configs[2])",
+                   "shapes_din_dout": SHAPES, "tokens_per_worker": T, "workers": P,
+                   "scheme": "quest fwd / rtn bwd, hadamard g=32", "implementation":
+                   "mx4train.qlinear.forward/backward from baseline/_ref (unmodified reference, native backend)"},
+        "cpu_baseline": {"value": round(v, 6), "unit": "TFLOP/s", "cores": P, "kind": "reference",
+                         "sample": f"per step one fwd+bwd of one shape (cycling) on {P} worker processes x {T} "
+                                   f"tokens (of the GPU arm's 16384), {done} steps timed"},
         "e2e": {"value": round(v, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -512,7 +578,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tokens", type=int, default=16384)
-    ap.add_argument("--ref-tokens", type=int, default=256)
+    ap.add_argument("--ref-tokens", type=int, default=256, help="reference arm: tokens per worker and step")
+    ap.add_argument("--ref-workers", type=int, default=0, help="reference arm: worker processes (0 = all cores)")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0, help="reference arm: wall-clock budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel from Python each step")
@@ -549,10 +617,10 @@ def main():
         if out is not None:
             out["train"] = tr
     if out is not None and world == 1 and not args.no_cpu_baseline:
-        r = cpu_baseline_sample(1, 128)
+        r = cpu_baseline_sample(128)
         out["cpu_baseline"] = {"value": round(r["flop"] / r["seconds"] / 1e12, 6), "unit": "TFLOP/s", "cores": 1,
-                               "kind": "port", "sample": "128 tokens x 3 shapes, one fwd+bwd each (oracle/, "
-                                                          "single-threaded like the reference's Cython kernels)",
+                               "kind": "reference", "sample": "128 tokens x 3 shapes, one fwd+bwd each through the "
+                               "unmodified mx4train.qlinear (baseline/_ref, native backend, single-threaded)",
                                "seconds": round(r["seconds"], 2)}
     if world > 1:
         dist.barrier()
