@@ -480,10 +480,15 @@ def run_train(rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     out = {"data": "synthetic token streams (no datasets offline)",
            "optimizer": "AdamW 0.9/0.95 wd 0.1, clip 1.0, warmup+cosine (train.py:58-85, 325-382)"}
-    out["llama200m_dp"] = run(llama, "200m", 64, 5, 2, False, dev, world, rank)
-    out["llama30m"] = run(llama, "30m", 64, 3, 1, False, dev, world, rank)
-    out["block7b_8k_b4"] = run(llama, "7b", 4, 3, 1, True, dev, world, rank)
-    torch.cuda.empty_cache()
+    for key, args in (("llama200m_dp", ("200m", 64, 5, 2, False)), ("llama30m", ("30m", 64, 3, 1, False)),
+                      ("block7b_8k_b4", ("7b", 4, 3, 1, True))):
+        q = run(llama, *args, dev, world, rank, "quartet")
+        torch.cuda.empty_cache()
+        b = run(llama, *args, dev, world, rank, "bf16")   # comparator: same model/glue/optimizer, bf16 linears
+        torch.cuda.empty_cache()
+        q["bf16_arm"] = {k: b[k] for k in ("ms_per_step", "tokens_per_s", "linear_tflops", "loss") if k in b}
+        q["speedup_vs_bf16"] = round(b["ms_per_step"] / q["ms_per_step"], 3)
+        out[key] = q
     return out
 
 

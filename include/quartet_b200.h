@@ -9,8 +9,10 @@
  *
  * Conventions (all functions):
  *   - plain device pointers, sizes in elements unless a name says bytes; no allocation, no throw;
- *   - stream-ordered on the caller's `stream` (a cudaStream_t passed as void*); reentrant, no
- *     global mutable state beyond a lazily resolved driver entry point;
+ *   - stream-ordered on the caller's `stream` (a cudaStream_t passed as void*); reentrant.  Process
+ *     state: a lazily resolved driver entry point, per-device caches of launch facts (SM count,
+ *     occupancy, one-time kernel attributes; any device of the process may be current), and the
+ *     qt_debug_set_* test knobs (production value 0, never set by the product path);
  *   - return 0 on success, a cudaError_t value (1..999) on a CUDA error, or a QT_ERR_* code;
  *   - `err` (nullable, device int) gets bit 0 set when a quantizer sees a non-finite input: the
  *     analogue of the reference's ValueError("non-finite input") (codec.py:164-170), checked by
@@ -192,6 +194,10 @@ QT_API void qt_debug_set_gemm(int dbg);
  * experimental, about par with the CUDA-core kernel); `fallbacks` (nullable device ints: 1 for mode 0,
  * 3 for mode 3) counts groups a tensor-core path re-decided exactly.  Not thread-safe; tests only. */
 QT_API void qt_debug_set_quant(int mode, int* fallbacks);
+/* Parity-test hook: cap every persistent grid (quantizer and GEMM kernels) at max_ctas CTAs (the 2-CTA GEMM
+ * at max_ctas/2 pairs, at least one), so that each CTA walks many tiles; 0 restores the production grid.
+ * Not thread-safe; tests only. */
+QT_API void qt_debug_set_grid(int max_ctas);
 
 /* ---- Llama-loop glue (not on the Quartet path; llama.py): fused bf16 elementwise kernels, fp32 math.
  * qt_rope: half-split rotary embedding of x [batch, seq, heads, head_dim] (rows = batch * seq; element

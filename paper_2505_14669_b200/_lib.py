@@ -33,6 +33,7 @@ SIGNATURES = {
     "qt_sign_bits_at": (_i32, [_vp, _i64, _i64, _u64, _vp]),
     "qt_sign_bits_pair": (_i32, [_vp, _i64, _i64, _vp, _i64, _i64, _u64, _vp]),
     "qt_debug_set_gemm": (None, [_i32]),
+    "qt_debug_set_grid": (None, [_i32]),
     "qt_debug_set_quant": (None, [_i32, _vp]),
     "qt_rope": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _i32, _i64, _i64, _i64, _vp]),
     "qt_swiglu": (_i32, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp]),

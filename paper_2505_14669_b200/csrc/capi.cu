@@ -13,7 +13,35 @@ static int g_gemm_dbg = 0;  // experiment knobs for qt_debug_set_gemm (never set
 static int g_quant_mode = 0;  // qt_debug_set_quant: 0 production, 1 CUDA cores only, 3 tensor-core QuEST forward
 static int* g_quant_fallbacks = nullptr;
 
+namespace qt {
+int g_grid_cap = 0;
+
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev < 0 || dev >= kMaxDevices ? 0 : dev;
+}
+int device_sms() {
+    static int sms[kMaxDevices];  // 0 = not yet queried (a benign race: every writer stores the same value)
+    const int dev = current_device();
+    if (!sms[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        sms[dev] = n > 0 ? n : 148;
+    }
+    return sms[dev];
+}
+bool first_use_on_device(int (&flags)[kMaxDevices]) {
+    const int dev = current_device();
+    if (flags[dev]) return false;
+    flags[dev] = 1;
+    return true;
+}
+}  // namespace qt
+
 extern "C" {
+
+void qt_debug_set_grid(int max_ctas) { qt::g_grid_cap = max_ctas > 0 ? max_ctas : 0; }
 
 void qt_debug_set_gemm(int dbg) {
     g_gemm_dbg = dbg & 0xFFFF;

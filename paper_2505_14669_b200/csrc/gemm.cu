@@ -13,6 +13,8 @@
 //                EPI_MASK_H     trust-mask multiply, in-register FWHT-32 along N, x scale
 //                EPI_MASK       trust-mask multiply, x scale (hadamard=False layers)
 //                               (qlinear.py:229-230 / 249-250: dx = H(dx_q * m_x) * 16/9)
+#include <algorithm>
+
 #include "common.cuh"
 #include "launch.h"
 #include "quant.cuh"  // Pair / fwht_pair / scale_pair (bit-exact packed FWHT-32)
@@ -706,15 +708,12 @@ static int launch_gemm_bn(const uint8_t* a, int64_t lda, const uint8_t* a_sf, in
     if (rc) return rc;
     rc = make_codes_map(&tb, b, N, K / 2, ldb, BN);
     if (rc) return rc;
-    static int sms = 0;
-    if (!sms) {
+    static int attr_set[kMaxDevices];
+    if (first_use_on_device(attr_set))
         cudaFuncSetAttribute(k_gemm_mxf4<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int64_t sms = device_sms();
     const int64_t tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
-    const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
+    const unsigned grid = (unsigned)cap_grid(tiles < sms ? tiles : sms);
     k_gemm_mxf4<BN><<<grid, kThreads, L::BYTES, st>>>(ta, tb, a_sf, a_katoms, b_sf, b_katoms, (int)M, (int)N, (int)K,
                                                       ep);
     return (int)cudaGetLastError();
@@ -740,7 +739,8 @@ int g_gemm_cluster8 = 0;  // 1: clusters of 4 pairs with TMA multicast (measured
 template <int NP>
 static int launch_2sm_np(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tsa, const CUtensorMap& tsb,
                          const CUtensorMap& to, int64_t M, int64_t N, int64_t K, const EpiParams& ep, cudaStream_t st) {
-    static int max_clusters = 0;
+    static int max_clusters_dev[kMaxDevices];
+    int& max_clusters = max_clusters_dev[current_device()];
     if (!max_clusters) {
         cudaFuncSetAttribute(k_gemm_mxf4_2sm<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm2::kBytes);
         if (NP == 4) cudaFuncSetAttribute(k_gemm_mxf4_2sm<NP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
@@ -758,16 +758,14 @@ static int launch_2sm_np(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
         int n = 0;
         if (cudaOccupancyMaxActiveClusters(&n, k_gemm_mxf4_2sm<NP>, &cfg) != cudaSuccess || n <= 0) {
             cudaGetLastError();
-            int dev = 0, sms = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            n = sms / (2 * NP);
+            n = device_sms() / (2 * NP);
         }
         max_clusters = n;
     }
     const int64_t tm = (M + 255) / 256, tn = (N + 255) / 256;
     const int64_t tiles = NP == 4 ? ((tm + 1) / 2) * ((tn + 1) / 2) : tm * tn;
-    const int64_t clusters = tiles < max_clusters ? tiles : max_clusters;
+    int64_t clusters = tiles < max_clusters ? tiles : max_clusters;
+    if (g_grid_cap > 0) clusters = std::max<int64_t>(1, std::min<int64_t>(clusters, g_grid_cap / (2 * NP)));
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

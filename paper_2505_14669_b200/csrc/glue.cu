@@ -7,6 +7,7 @@
 #include <math.h>
 
 #include "../../include/quartet_b200.h"
+#include "launch.h"
 
 namespace {
 
@@ -353,12 +354,7 @@ __global__ void __launch_bounds__(256) k_rmsnorm_wide(const uint4* __restrict__ 
 }
 
 int grid_for(int64_t work) {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int64_t sms = qt::device_sms();
     const int64_t blocks = (work + 255) / 256;
     return (int)(blocks < (int64_t)sms * 8 ? blocks : (int64_t)sms * 8);
 }
@@ -430,9 +426,7 @@ QT_API int qt_cross_entropy(const void* logits, const int64_t* targets, int64_t 
     if (rows < 0 || vocab <= 0 || vocab % 8 != 0) return QT_ERR_SHAPE;
     if (!al16(logits) || (backward && !al16(dlogits))) return QT_ERR_ALIGN;
     if (rows == 0) return 0;
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t sms = qt::device_sms();
     const int64_t blocks = rows < (int64_t)sms * 8 ? rows : (int64_t)sms * 8;
     k_xent<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint4*>(logits), targets, lse, loss,
                                                                static_cast<uint4*>(dlogits), dloss, scale, rows,

@@ -48,6 +48,17 @@ struct EpiParams {
     int accumulate;          // D += epilogue result (rounded to D's dtype first), QT_EPI_ACCUMULATE
 };
 
+// ---- per-device launch facts (the library serves any device of the process; no single-device caches)
+constexpr int kMaxDevices = 64;
+int current_device();
+int device_sms();                       // SM count of the current device (cached per device)
+// true exactly once per device for the given flag array (one-time cudaFuncSetAttribute per device)
+bool first_use_on_device(int (&flags)[kMaxDevices]);
+// qt_debug_set_grid: cap on the persistent grid of every tile kernel (0 = no cap, production).  Tests set a
+// small cap so that each CTA walks many tiles (multi-tile pipelines, stage reuse, TMEM phases).
+extern int g_grid_cap;
+inline int64_t cap_grid(int64_t want) { return g_grid_cap > 0 && want > g_grid_cap ? g_grid_cap : want; }
+
 int launch_transform_rows(const float* x, float* out, int64_t rows, int64_t cols, int transform,
                           const uint32_t* sign_bits, float prescale, cudaStream_t st);
 int launch_signs(uint32_t* bits, int64_t start, int64_t n, uint64_t xi, cudaStream_t st);

@@ -507,17 +507,17 @@ template <int IN, int ROW, int COL, int CROUND>
 static int quant_launch(const TileArgs& a, cudaStream_t st) {
     using G = Geom<IN>;
     auto fn = k_quant<IN, ROW, COL, CROUND>;
-    static int ctas = 0;
-    if (!ctas) {
+    static int per_sm[kMaxDevices];
+    const int dev = current_device();
+    if (!per_sm[dev]) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, G::BYTES);
-        int dev = 0, sms = 148, per_sm = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, G::BYTES);
-        ctas = sms * (per_sm > 0 ? per_sm : 1);
+        int n = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, 256, G::BYTES);
+        per_sm[dev] = n > 0 ? n : 1;
     }
+    const int64_t ctas = (int64_t)device_sms() * per_sm[dev];
     const int64_t tiles = ((a.R + G::TR - 1) / G::TR) * ((a.C + kTC - 1) / kTC);
-    const unsigned n = (unsigned)(tiles < ctas ? tiles : ctas);
+    const unsigned n = (unsigned)cap_grid(tiles < ctas ? tiles : ctas);
     fn<<<n, 256, G::BYTES, st>>>(a);
     return 0;
 }

@@ -271,16 +271,13 @@ int launch_tcq_dual(const void* x, int64_t ldx, int64_t R, int64_t C, const uint
     CUtensorMap m;
     const int rc = tq_map(&m, x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R, C, ldx * 2);
     if (rc) return rc;
-    static int sms = 0;
-    if (!sms) {
+    static int attr_set[kMaxDevices];
+    if (first_use_on_device(attr_set))
         cudaFuncSetAttribute(k_tcq_dual, cudaFuncAttributeMaxDynamicSharedMemorySize, kTqBytes);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int64_t sms = device_sms();
     TqArgs a{R, C, row_sign_bits, col_sign_bits, row_out, col_out, prescale, fallbacks, g_tcq_dbg};
     const int64_t tiles = ((R + 127) / 128) * ((C + 127) / 128);
-    const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
+    const unsigned grid = (unsigned)cap_grid(tiles < sms ? tiles : sms);
     k_tcq_dual<<<grid, kTqThreads, kTqBytes, st>>>(m, a);
     return (int)cudaGetLastError();
 }

@@ -469,16 +469,13 @@ int launch_tcq_xq(const void* x, int64_t ldx, int64_t R, int64_t C, const QuantO
     CUtensorMap m;
     const int rc = tq_map(&m, x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R, C, ldx * 2);
     if (rc) return rc;
-    static int sms = 0;
-    if (!sms) {
+    static int attr_set[kMaxDevices];
+    if (first_use_on_device(attr_set))
         cudaFuncSetAttribute(k_tcq_xq, cudaFuncAttributeMaxDynamicSharedMemorySize, kXqBytes);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int64_t sms = device_sms();
     XqArgs a{R, C, row_out, col_sign_bits, col_out, col_prescale, fallbacks, g_tcq_dbg};
     const int64_t tiles = ((R + 127) / 128) * ((C + 127) / 128);
-    k_tcq_xq<<<(unsigned)(tiles < sms ? tiles : sms), kXqThreads, kXqBytes, st>>>(m, a);
+    k_tcq_xq<<<(unsigned)cap_grid(tiles < sms ? tiles : sms), kXqThreads, kXqBytes, st>>>(m, a);
     return (int)cudaGetLastError();
 }
 

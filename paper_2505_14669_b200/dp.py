@@ -41,18 +41,3 @@ def allreduce_dw(dw: torch.Tensor, group=None, comm_dtype: torch.dtype | None = 
     dist.all_reduce(buf, group=group)
     dw.copy_(buf)
     return dw
-
-
-class ShardContext:
-    """Token-shard placement consulted by QuartetLinear's backward (set once per step)."""
-
-    offset: int = 0
-    total: int | None = None
-
-    @classmethod
-    def set(cls, offset: int, total: int | None) -> None:
-        cls.offset, cls.total = int(offset), (None if total is None else int(total))
-
-    @classmethod
-    def clear(cls) -> None:
-        cls.offset, cls.total = 0, None

@@ -26,7 +26,7 @@ import torch.nn.functional as F
 
 from . import _lib
 from .mxfp4 import _stream
-from .nn import QuartetLinear, quartet_linear_group
+from .nn import QuartetLinear, quartet_linear_group, set_token_shard
 
 GROUP = 32
 
@@ -41,6 +41,7 @@ class LlamaConfig:
     d_ff: int | None = None          # SwiGLU hidden size; default 8/3 d rounded up to 256
     rounding: str = "rtn"
     rope_base: float = 10000.0
+    linear: str = "quartet"          # "quartet" (MXFP4, the product) or "bf16" (the comparator arm)
 
     @property
     def hidden(self) -> int:
@@ -206,6 +207,34 @@ def rope(x, cos, sin):
     return _Rope.apply(x, cos[: x.shape[1]], sin[: x.shape[1]])
 
 
+class Bf16Linear(torch.nn.Module):
+    """The comparator arm of the training benchmarks: a bias-free linear with the same fp32 master weight
+    and initialisation as QuartetLinear, computed as a bf16 cuBLAS matmul (standard bf16 mixed precision,
+    the paper's BF16 baseline).  Everything else in the model is shared with the Quartet arm."""
+
+    def __init__(self, in_features: int, out_features: int, device=None):
+        super().__init__()
+        self.weight = torch.nn.Parameter(torch.empty(out_features, in_features, device=device))
+        torch.nn.init.normal_(self.weight, std=1.0 / math.sqrt(in_features))
+
+    def forward(self, x):
+        return F.linear(x, self.weight.to(x.dtype))
+
+
+def make_linear(cfg: LlamaConfig, i: int, o: int, seed: int, layer_id: int, device=None):
+    if cfg.linear == "bf16":
+        return Bf16Linear(i, o, device=device)
+    if cfg.linear != "quartet":
+        raise ValueError(f"unknown linear kind {cfg.linear!r}")
+    return QuartetLinear(i, o, seed=seed, layer_id=layer_id, rounding=cfg.rounding, device=device)
+
+
+def linear_group(x, mods):
+    if isinstance(mods[0], QuartetLinear):
+        return quartet_linear_group(x, mods)
+    return tuple(m(x) for m in mods)
+
+
 class Block(torch.nn.Module):
     def __init__(self, cfg: LlamaConfig, index: int, seed: int, device=None):
         super().__init__()
@@ -213,7 +242,7 @@ class Block(torch.nn.Module):
         lid = 16 * index
 
         def ql(i, o, k):
-            return QuartetLinear(i, o, seed=seed, layer_id=lid + k, rounding=cfg.rounding, device=device)
+            return make_linear(cfg, i, o, seed, lid + k, device)
 
         self.n_head = cfg.n_head
         self.attn_norm, self.mlp_norm = RMSNorm(d, device=device), RMSNorm(d, device=device)
@@ -224,14 +253,14 @@ class Block(torch.nn.Module):
         B, S, d = x.shape
         H, dh = self.n_head, d // self.n_head
         a = self.attn_norm(x)
-        q, k, v = quartet_linear_group(a, (self.q, self.k, self.v))  # one QuEST read of a for q/k/v
+        q, k, v = linear_group(a, (self.q, self.k, self.v))  # one QuEST read of a for q/k/v
         q = rope(q.view(B, S, H, dh), cos, sin).transpose(1, 2)
         k = rope(k.view(B, S, H, dh), cos, sin).transpose(1, 2)
         v = v.view(B, S, H, dh).transpose(1, 2)
         att = F.scaled_dot_product_attention(q, k, v, is_causal=True)
         x = x + self.o(att.transpose(1, 2).reshape(B, S, d))
         m = self.mlp_norm(x)
-        g, u = quartet_linear_group(m, (self.gate, self.up))
+        g, u = linear_group(m, (self.gate, self.up))
         return x + self.down(swiglu(g, u))
 
 
@@ -246,8 +275,7 @@ class LlamaQuartet(torch.nn.Module):
             (torch.randn(cfg.vocab, cfg.d_model, generator=g) * 0.02).to(device))
         self.blocks = torch.nn.ModuleList(Block(cfg, i, seed, device) for i in range(cfg.n_layer))
         self.norm = RMSNorm(cfg.d_model, device=device)
-        self.head = None if blocks_only else QuartetLinear(cfg.d_model, cfg.vocab, seed=seed, layer_id=16 * 4096,
-                                                           rounding=cfg.rounding, device=device)
+        self.head = None if blocks_only else make_linear(cfg, cfg.d_model, cfg.vocab, seed, 16 * 4096, device)
         cos, sin = _rope(cfg.seq_len, cfg.d_model // cfg.n_head, cfg.rope_base, device)
         self.register_buffer("cos", cos, persistent=False)
         self.register_buffer("sin", sin, persistent=False)
@@ -383,8 +411,24 @@ class Trainer:
                                      fused=params[0].is_cuda)
         self.bucket = OverlappedGradBuckets(params)
         self.step_i = 0
+        self._shard_tokens = None
+
+    def _place_shard(self, n_tokens: int) -> None:
+        """Data parallel: rank r holds sequences [r B, (r+1) B) of the global batch, i.e. tokens
+        [r n, (r+1) n) -- its Quartet layers use the global token offset, so the
+        ranks together reproduce the single-GPU step on the concatenated batch."""
+        import torch.distributed as dist
+
+        if self._shard_tokens == n_tokens:
+            return
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            set_token_shard(self.model, dist.get_rank() * n_tokens, dist.get_world_size() * n_tokens)
+        else:
+            set_token_shard(self.model, 0, None)
+        self._shard_tokens = n_tokens
 
     def step(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        self._place_shard(tokens.numel())
         lr = lr_at(self.step_i, self.steps, self.lr)
         for gr in self.opt.param_groups:
             gr["lr"] = lr

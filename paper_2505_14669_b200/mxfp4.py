@@ -185,12 +185,13 @@ def quant_cols(x, rounding: int, *, transform: int, signs: torch.Tensor | None =
 
 def quant_fused(x: torch.Tensor, rounding: int, col_rounding: int, *, transform: int, col_transform: int,
                 col_signs: torch.Tensor | None = None, prescale: float = 1.0, col_prescale: float = 0.75,
-                sr_seed: int = 0, col_seed: int = 0, col_counter_start: int = 0, col_counter_ld: int = 0,
-                want_mask: bool = True, err: torch.Tensor | None = None, fallbacks: torch.Tensor | None = None):
+                sr_seed: int = 0, counter_start: int = 0, col_seed: int = 0, col_counter_start: int = 0,
+                col_counter_ld: int = 0, want_mask: bool = True, err: torch.Tensor | None = None, fallbacks: torch.Tensor | None = None):
     """A forward operand and its transposed backward requantization from ONE read of x[rows, cols]
     (qt_quant_fused): returns (row operand [rows, cols] = Q(T(x)), col operand [cols, rows] =
     Q_col(T_col(deq(row operand)^T) * col_prescale)), i.e. (X_q, X_t) or (W_q, W_t) of qlinear.py:139-157
-    and 206-207 / 215 / 235.  `col_signs` flips the row axis (the backward contraction axis)."""
+    and 206-207 / 215 / 235.  `col_signs` flips the row axis (the backward contraction axis).  counter_start:
+    SR stream position of the row operand's element (0, 0) (row shard r0 of a [R, cols] matrix: r0 * cols)."""
     _require_cuda(x, "x")
     if x.stride(1) != 1:
         x = x.contiguous()
@@ -200,7 +201,7 @@ def quant_fused(x: torch.Tensor, rounding: int, col_rounding: int, *, transform:
     r_op = MXOperand.empty(rows, cols, x.device, with_mask=want_mask)
     c_op = MXOperand.empty(cols, rows, x.device)
     rc = _lib.load().qt_quant_fused(x.data_ptr(), _in_dtype(x), x.stride(0), rows, cols, transform, None,
-                                    float(prescale), rounding, int(sr_seed) & 0xFFFFFFFFFFFFFFFF, 0, 0,
+                                    float(prescale), rounding, int(sr_seed) & 0xFFFFFFFFFFFFFFFF, int(counter_start), 0,
                                     r_op.codes.data_ptr(), r_op.codes.stride(0), r_op.sf.data_ptr(), r_op.katoms,
                                     r_op.mask.data_ptr() if r_op.mask is not None else None, col_transform,
                                     col_signs.data_ptr() if col_signs is not None else None, float(col_prescale),

@@ -23,18 +23,17 @@ from .mxfp4 import derive_seed
 class QuartetLinearFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, xi: int, rounding: str = "rtn", hadamard: bool = True,
-                scheme: qlinear.QuantScheme = qlinear.QUEST):
+                scheme: qlinear.QuantScheme = qlinear.QUEST, shard: tuple = (0, None)):
         lead = x.shape[:-1]
         x2 = x.reshape(-1, x.shape[-1])
         if x2.dtype not in (torch.bfloat16, torch.float32):
             x2 = x2.float()
-        from .dp import ShardContext
-
+        ctx.shard = shard
         # xi is known now, so X_t / W_t come out of the same read of x / w (qt_quant_fused)
         y, lctx = qlinear.forward(x2, w.detach(), scheme=scheme, hadamard=hadamard, seed=xi,
                                   out_dtype=x.dtype if x.dtype in (torch.bfloat16, torch.float32) else torch.float32,
                                   check_finite=False, bwd_xi=int(xi), bwd_rounding=rounding,
-                                  token_offset=ShardContext.offset, total_tokens=ShardContext.total)
+                                  token_offset=shard[0], total_tokens=shard[1])
         ctx.lctx = lctx
         ctx.xi = int(xi)
         ctx.rounding = rounding
@@ -48,14 +47,12 @@ class QuartetLinearFn(torch.autograd.Function):
         dy2 = dy.reshape(-1, dy.shape[-1])
         if dy2.dtype not in (torch.bfloat16, torch.float32):
             dy2 = dy2.float()
-        from .dp import ShardContext
-
         dx, dw = qlinear.backward(dy2, ctx.lctx, ctx.xi, ctx.rounding, dx_dtype=ctx.x_dtype
                                   if ctx.x_dtype in (torch.bfloat16, torch.float32) else torch.float32,
-                                  dw_dtype=torch.float32, check_finite=False, token_offset=ShardContext.offset,
-                                  total_tokens=ShardContext.total)
+                                  dw_dtype=torch.float32, check_finite=False, token_offset=ctx.shard[0],
+                                  total_tokens=ctx.shard[1])
         ctx.lctx = None
-        return dx.reshape(ctx.x_shape), dw.to(ctx.w_dtype), None, None, None, None
+        return dx.reshape(ctx.x_shape), dw.to(ctx.w_dtype), None, None, None, None, None
 
 
 class QuartetLinearGroupFn(torch.autograd.Function):
@@ -65,20 +62,19 @@ class QuartetLinearGroupFn(torch.autograd.Function):
     Outputs and weight gradients are bit-identical to separate QuartetLinearFn calls."""
 
     @staticmethod
-    def forward(ctx, x, xis, rounding, hadamard, scheme, *ws):
+    def forward(ctx, x, xis, rounding, hadamard, scheme, shard, *ws):
         lead = x.shape[:-1]
         x2 = x.reshape(-1, x.shape[-1])
         if x2.dtype not in (torch.bfloat16, torch.float32):
             x2 = x2.float()
-        from .dp import ShardContext
-
+        ctx.shard = shard
         x_q = qlinear.quantize_operand(x2, scheme, hadamard)
         out_dtype = x.dtype if x.dtype in (torch.bfloat16, torch.float32) else torch.float32
         ys, ctx.lctxs = [], []
         for w, xi in zip(ws, xis):
             y, lctx = qlinear.forward(x2, w.detach(), scheme=scheme, hadamard=hadamard, out_dtype=out_dtype,
                                       check_finite=False, bwd_xi=int(xi), bwd_rounding=rounding,
-                                      token_offset=ShardContext.offset, total_tokens=ShardContext.total, x_q=x_q)
+                                      token_offset=shard[0], total_tokens=shard[1], x_q=x_q)
             ys.append(y.reshape(*lead, w.shape[0]))
             ctx.lctxs.append(lctx)
         ctx.xis, ctx.rounding, ctx.x_shape, ctx.x_dtype = [int(v) for v in xis], rounding, x.shape, x.dtype
@@ -87,8 +83,6 @@ class QuartetLinearGroupFn(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, *dys):
-        from .dp import ShardContext
-
         dx_dtype = ctx.x_dtype if ctx.x_dtype in (torch.bfloat16, torch.float32) else torch.float32
         dx_sum, dws = None, []
         for dy, lctx, xi, wdt in zip(dys, ctx.lctxs, ctx.xis, ctx.w_dtypes):
@@ -99,30 +93,43 @@ class QuartetLinearGroupFn(torch.autograd.Function):
             # epilogue adding into the first layer's dx (QT_EPI_ACCUMULATE): no separate add pass
             dx_sum, dw = qlinear.backward(dy2.contiguous(), lctx, xi, ctx.rounding, dx_dtype=dx_dtype,
                                           dw_dtype=torch.float32, check_finite=False,
-                                          token_offset=ShardContext.offset, total_tokens=ShardContext.total,
+                                          token_offset=ctx.shard[0], total_tokens=ctx.shard[1],
                                           dx_accumulate=dx_sum)
             dws.append(dw.to(wdt))
         ctx.lctxs = None
-        return (dx_sum.reshape(ctx.x_shape), None, None, None, None, *dws)
+        return (dx_sum.reshape(ctx.x_shape), None, None, None, None, None, *dws)
 
 
 def quartet_linear_group(x, mods):
     """Apply QuartetLinear modules that share the input x with one forward quantization of x."""
     m0 = mods[0]
     if (m0.scheme.kind == "sr_absmax" or any(m.rounding != m0.rounding or m.hadamard != m0.hadamard
-                                             or m.scheme is not m0.scheme for m in mods)):
+                                             or m.scheme is not m0.scheme or m.token_shard != m0.token_shard
+                                             for m in mods)):
         return tuple(m(x) for m in mods)
     xis = []
     for m in mods:
         xis.append(m.xi())
         if m.training:
             m.step += 1
-    return QuartetLinearGroupFn.apply(x, xis, m0.rounding, m0.hadamard, m0.scheme, *[m.weight for m in mods])
+    return QuartetLinearGroupFn.apply(x, xis, m0.rounding, m0.hadamard, m0.scheme, m0.token_shard,
+                                      *[m.weight for m in mods])
 
 
 def quartet_linear(x, w, xi: int, rounding: str = "rtn", hadamard: bool = True,
-                   scheme: qlinear.QuantScheme = qlinear.QUEST):
-    return QuartetLinearFn.apply(x, w, xi, rounding, hadamard, scheme)
+                   scheme: qlinear.QuantScheme = qlinear.QUEST, token_offset: int = 0,
+                   total_tokens: int | None = None):
+    return QuartetLinearFn.apply(x, w, xi, rounding, hadamard, scheme, (int(token_offset), total_tokens))
+
+
+def set_token_shard(model: torch.nn.Module, token_offset: int, total_tokens: int | None) -> None:
+    """Place every QuartetLinear of `model` on a data-parallel token shard: this rank's rows are tokens
+    [token_offset, token_offset + local) of a global batch of `total_tokens` (row = sequence * seq_len +
+    position).  Their token-axis randomized-Hadamard signs and stochastic-rounding stream positions are then
+    the single-GPU ones, so the ranks together compute the single-GPU step."""
+    for m in model.modules():
+        if isinstance(m, QuartetLinear):
+            m.token_shard = (int(token_offset), None if total_tokens is None else int(total_tokens))
 
 
 class QuartetLinear(torch.nn.Module):
@@ -139,6 +146,7 @@ class QuartetLinear(torch.nn.Module):
         self.seed, self.layer_id = int(seed), int(layer_id)
         self.rounding, self.hadamard, self.scheme = rounding, hadamard, scheme
         self.step = 0
+        self.token_shard: tuple = (0, None)   # (token offset, global tokens) of this rank: set_token_shard
         torch.nn.init.normal_(self.weight, std=1.0 / math.sqrt(in_features))
 
     def xi(self) -> int:
@@ -148,7 +156,7 @@ class QuartetLinear(torch.nn.Module):
         xi = self.xi()
         if self.training:
             self.step += 1
-        return QuartetLinearFn.apply(x, self.weight, xi, self.rounding, self.hadamard, self.scheme)
+        return QuartetLinearFn.apply(x, self.weight, xi, self.rounding, self.hadamard, self.scheme, self.token_shard)
 
     def extra_repr(self) -> str:
         return (f"in_features={self.in_features}, out_features={self.out_features}, "

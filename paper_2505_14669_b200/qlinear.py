@@ -150,15 +150,18 @@ def _raise_if_nonfinite(err: torch.Tensor | None) -> None:
 
 
 def quantize_operand(m: torch.Tensor, scheme: QuantScheme, hadamard: bool, seed: int | None = None,
-                     err: torch.Tensor | None = None) -> MXOperand:
-    """transform_last_axis + apply_scheme (qlinear.py:139-157) as one fused kernel."""
+                     err: torch.Tensor | None = None, row_offset: int = 0) -> MXOperand:
+    """transform_last_axis + apply_scheme (qlinear.py:139-157) as one fused kernel.  row_offset: the first
+    row's index in the full matrix (a data-parallel token shard), so that sr_absmax draws the single-GPU
+    stream positions (row * cols + col, quantizers.py:79-84)."""
     transform = _lib.QT_TRANSFORM_HADAMARD if hadamard else _lib.QT_TRANSFORM_NONE
     if scheme.kind == "quest":
         return quant_rows(m, transform, _lib.QT_ROUND_QUEST, want_mask=True, err=err)
     if scheme.kind == "rtn_absmax":
         op = quant_rows(m, transform, _lib.QT_ROUND_RTN, want_mask=True, err=err)
     else:
-        op = quant_rows(m, transform, _lib.QT_ROUND_SR, sr_seed=seed, want_mask=True, err=err)
+        op = quant_rows(m, transform, _lib.QT_ROUND_SR, sr_seed=seed, counter_start=row_offset * m.shape[1],
+                        want_mask=True, err=err)
     return op
 
 
@@ -211,8 +214,8 @@ def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, polic
         x_seed = derive_seed(bwd_xi, _TAG_BWD_X) if sr else 0
         if x_q is None:
             x_q, xt_q = quant_fused(x, row_rc, rc, transform=fwd_t, col_transform=bwd_t, col_signs=t_signs,
-                                    col_prescale=PRE_SCALE, sr_seed=sx or 0, col_seed=x_seed,
-                                    col_counter_start=token_offset, col_counter_ld=total, err=err)
+                                    col_prescale=PRE_SCALE, sr_seed=sx or 0, counter_start=token_offset * d_in,
+                                    col_seed=x_seed, col_counter_start=token_offset, col_counter_ld=total, err=err)
         else:  # shared X_q: this layer's X_t from its codes, as backward does without eager operands
             xt_q = quant_cols(x_q, rc, transform=bwd_t, signs=t_signs, prescale=PRE_SCALE, sr_seed=x_seed,
                               counter_start=token_offset, counter_ld=total, err=err)
@@ -221,8 +224,10 @@ def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, polic
                                 col_seed=derive_seed(bwd_xi, _TAG_BWD_W) if sr else 0, err=err)
         eager = _Eager(int(bwd_xi), bwd_rounding, int(token_offset), total, xt_q, wt_q, d_signs, t_signs)
     else:
+        if token_offset % g or token_offset < 0:
+            raise ValueError(f"token offset {token_offset} must be a non-negative multiple of {g}")
         if x_q is None:
-            x_q = quantize_operand(x, scheme, hadamard, sx, err)
+            x_q = quantize_operand(x, scheme, hadamard, sx, err, row_offset=token_offset)
         w_q = quantize_operand(w, scheme, hadamard, sw, err)
     y = gemm(x_q, w_q, out_dtype=out_dtype)
     _raise_if_nonfinite(err)

@@ -94,7 +94,7 @@ def main():
     ref = _import_reference()
     from mx4train import codec, qlinear, rng, selftest
     from mx4train._backend import kernels
-    from mx4train.quantizers import QUEST, RTN_ABSMAX
+    from mx4train.quantizers import QUEST, RTN_ABSMAX, SR_ABSMAX
 
     # ------------------------------------------------------------------ rng
     seeds = [0, 1, 7, 123456789, 2**63 + 5, 2**64 - 1]
@@ -149,22 +149,28 @@ def main():
 
     # -------------------------------------------------------------- qlinear
     cases = [
-        # name, T, d_in, d_out, scheme, hadamard, rounding, xi, input scale of w
+        # name, T, d_in, d_out, scheme, hadamard, rounding, xi[, forward seed (sr_absmax, qlinear.py:148-154)]
         ("quest_rtn", 64, 128, 96, QUEST, True, "rtn", 7),
         ("quest_sr", 64, 128, 96, QUEST, True, "sr", 7),
         ("quest_rtn_t256", 256, 128, 96, QUEST, True, "rtn", 11),
         ("rtnfwd_rtn", 64, 64, 64, RTN_ABSMAX, True, "rtn", 3),
         ("quest_rtn_noh", 64, 64, 96, QUEST, False, "rtn", 5),
+        ("srfwd_sr", 64, 128, 96, SR_ABSMAX, True, "sr", 13, 99),
+        ("srfwd_rtn_t256", 256, 96, 128, SR_ABSMAX, True, "rtn", 17, 2**64 - 3),
     ]
-    for name, T, d_in, d_out, scheme, had, rounding, xi in cases:
+    for name, T, d_in, d_out, scheme, had, rounding, xi, *fseed in cases:
+        if os.environ.get("GOLDEN_ONLY") and name not in os.environ["GOLDEN_ONLY"].split(","):
+            continue
+        seed = fseed[0] if fseed else None
         r = np.random.default_rng(zlib.crc32(name.encode()))
         x = bf16_values(r.normal(size=(T, d_in)).astype(np.float32))
         w = bf16_values((r.normal(size=(d_out, d_in)) / np.sqrt(d_in)).astype(np.float32))
         dy = bf16_values(r.normal(size=(T, d_out)).astype(np.float32))
-        y, ctx = qlinear.forward(x, w, scheme=scheme, hadamard=had)
+        y, ctx = qlinear.forward(x, w, scheme=scheme, hadamard=had, seed=seed)
         dx, dw = qlinear.backward(dy, ctx, xi=xi, rounding=rounding)
+        extra = {} if seed is None else {"seed": np.uint64(seed)}
         np.savez_compressed(
-            os.path.join(HERE, f"qlinear_{name}.npz"),
+            os.path.join(HERE, f"qlinear_{name}.npz"), **extra,
             x=x, w=w, dy=dy, xi=np.uint64(xi), scheme=scheme.kind, hadamard=had,
             rounding=rounding, y=y, dx=dx, dw=dw,
             x_codes=ctx.x_q.codes, x_scales=ctx.x_q.scales,

@@ -16,6 +16,7 @@ from gpu_util import assert_operand_equal, bf16_values, rel_err, to_dev
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 TOL = 1e-5
+GOLDEN_CASES = ["quest_rtn", "quest_sr", "quest_rtn_t256", "rtnfwd_rtn", "quest_rtn_noh", "srfwd_sr", "srfwd_rtn_t256"]
 
 
 @pytest.fixture(scope="module")
@@ -31,14 +32,17 @@ def _scheme(qt, kind):
 
 
 @pytest.mark.parametrize("eager", [False, True], ids=["lazy", "eager"])
-@pytest.mark.parametrize("case", ["quest_rtn", "quest_sr", "quest_rtn_t256", "rtnfwd_rtn", "quest_rtn_noh"])
+@pytest.mark.parametrize("case", GOLDEN_CASES)
 def test_golden_end_to_end(qt, oracle, case, eager):
-    """eager: forward(..., bwd_xi=xi) builds X_t / W_t in the forward read (qt_quant_fused)."""
+    """eager: forward(..., bwd_xi=xi) builds X_t / W_t in the forward read (qt_quant_fused).
+    srfwd_*: the sr_absmax forward scheme (stochastic rounding of X and W with derive_seed(seed, 11/12),
+    qlinear.py:148-154, quantizers.py:79-84)."""
     z = np.load(os.path.join(GOLDEN, f"qlinear_{case}.npz"))
     had = bool(z["hadamard"])
+    seed = int(z["seed"]) if "seed" in z.files else None
     kw = dict(bwd_xi=int(z["xi"]), bwd_rounding=str(z["rounding"])) if eager else {}
     y, ctx = qt.forward(to_dev(z["x"], torch.bfloat16), to_dev(z["w"], torch.bfloat16),
-                        scheme=_scheme(qt, str(z["scheme"])), hadamard=had, **kw)
+                        scheme=_scheme(qt, str(z["scheme"])), hadamard=had, seed=seed, **kw)
     assert (ctx.eager is not None) == eager
     # saved context: bit-exact against the reference's LayerContext
     assert np.array_equal(ctx.x_q.codes.cpu().numpy(), z["x_codes"])
@@ -53,7 +57,7 @@ def test_golden_end_to_end(qt, oracle, case, eager):
     assert rel_err(dx.cpu().numpy(), z["dx"]) <= TOL, rel_err(dx.cpu().numpy(), z["dx"])
     assert rel_err(dw.cpu().numpy(), z["dw"]) <= TOL, rel_err(dw.cpu().numpy(), z["dw"])
     # backward operands: bit-exact against the oracle's recomposition (itself pinned to the reference)
-    _, octx = oracle.forward(z["x"], z["w"], scheme=str(z["scheme"]), hadamard=had)
+    _, octx = oracle.forward(z["x"], z["w"], scheme=str(z["scheme"]), hadamard=had, seed=seed)
     oracle.backward(z["dy"], octx, xi=int(z["xi"]), rounding=str(z["rounding"]))
     for name, key in (("g_q", "gq"), ("wt_q", "wtq"), ("gt_q", "gtq"), ("xt_q", "xtq")):
         c, s = octx.inter[key]

@@ -73,13 +73,14 @@ def test_threads_do_not_change_results(oracle, golden_dir):
         assert np.array_equal(a, b)
 
 
-CASES = ["quest_rtn", "quest_sr", "quest_rtn_t256", "rtnfwd_rtn", "quest_rtn_noh"]
+CASES = ["quest_rtn", "quest_sr", "quest_rtn_t256", "rtnfwd_rtn", "quest_rtn_noh", "srfwd_sr", "srfwd_rtn_t256"]
 
 
 @pytest.mark.parametrize("case", CASES)
 def test_qlinear_end_to_end(oracle, golden_dir, case):
     z = _load(golden_dir, f"qlinear_{case}.npz")
-    y, ctx = oracle.forward(z["x"], z["w"], scheme=str(z["scheme"]), hadamard=bool(z["hadamard"]))
+    seed = int(z["seed"]) if "seed" in z.files else None   # sr_absmax forward (qlinear.py:148-154)
+    y, ctx = oracle.forward(z["x"], z["w"], scheme=str(z["scheme"]), hadamard=bool(z["hadamard"]), seed=seed)
     assert np.array_equal(oracle.pack_nibbles(ctx.x_codes), z["x_codes"])
     assert np.array_equal(ctx.x_scales, z["x_scales"])
     assert np.array_equal(oracle.pack_nibbles(ctx.w_codes), z["w_codes"])

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--block", action="store_true", help="one transformer block (fwd+bwd), no embedding/head")
+    ap.add_argument("--linear", default="quartet", choices=["quartet", "bf16"])
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -34,17 +35,19 @@ def main():
         dist.init_process_group("nccl")
     qt.load()
     dev = torch.device("cuda", local)
-    print(json.dumps(run(llama, a.preset, a.batch, a.steps, a.warmup, a.block, dev, world, rank)) if rank == 0 else "",
+    print(json.dumps(run(llama, a.preset, a.batch, a.steps, a.warmup, a.block, dev, world, rank, a.linear)) if rank == 0 else "",
           flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def run(llama, preset, batch, steps, warmup, block, dev, world=1, rank=0):
+def run(llama, preset, batch, steps, warmup, block, dev, world=1, rank=0, linear="quartet"):
+    """linear: "quartet" (every linear MXFP4 through libquartet_b200) or "bf16" (the comparator arm: the
+    same model, glue kernels, optimizer and data with bf16 cuBLAS linears)."""
     import torch
     import torch.distributed as dist
 
-    cfg = llama.PRESETS[preset]
+    cfg = llama.LlamaConfig(**{**llama.PRESETS[preset].__dict__, "linear": linear})
     if block:
         cfg = llama.LlamaConfig(**{**cfg.__dict__, "n_layer": 1})
     model = llama.LlamaQuartet(cfg, seed=0, device=dev, blocks_only=block)
@@ -80,7 +83,7 @@ def run(llama, preset, batch, steps, warmup, block, dev, world=1, rank=0):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     lin = cfg.n_layer * (4 * cfg.d_model ** 2 + 3 * cfg.d_model * cfg.hidden) + (0 if block else cfg.d_model * cfg.vocab)
-    out = {"preset": preset, "block_only": block, "n_layer": cfg.n_layer, "d_model": cfg.d_model,
+    out = {"preset": preset, "linear": linear, "block_only": block, "n_layer": cfg.n_layer, "d_model": cfg.d_model,
            "seq_len": cfg.seq_len, "seqs_per_gpu": batch, "n_gpus": world, "ms_per_step": round(ms, 3),
            "tokens_per_s": round(world * tokens / (ms * 1e-3), 1),
            "linear_tflops": round(world * 6 * tokens * lin / (ms * 1e-3) / 1e12, 1)}
