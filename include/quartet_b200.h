@@ -199,6 +199,35 @@ QT_API void qt_debug_set_quant(int mode, int* fallbacks);
  * Not thread-safe; tests only. */
 QT_API void qt_debug_set_grid(int max_ctas);
 
+/* ---- exact plugin seam: every input the reference's kernels accept ---------------------------
+ * The reference's `kernels` module takes f64 matrices, any group size, any power-of-two FWHT block in f32
+ * or f64, and a fixed-order GEMM (_native.pyx:104-396).  These entry points replay it operation for
+ * operation in scalar f64 / f32 device code (one thread per group / block / output element), bit-identical
+ * for every input; the layer path uses the tiled kernels above.  Codes, masks and scales are UNPACKED,
+ * the reference's own layout: codes / mask uint8 [rows, cols], scales uint8 [rows, ceil(cols / group)].
+ *
+ * qt_seam_quantize: rounding QT_ROUND_RTN  -> quantize_rtn   (_native.pyx:104-131), codes + scales
+ *                            QT_ROUND_SR   -> quantize_sr    (_native.pyx:134-168), stream position
+ *                                             counter_start + i*cols + j of seed `seed`
+ *                            QT_ROUND_QUEST-> quantize_quest (_native.pyx:171-245, clip ratio ratio_lo), + mask
+ *   values != 0: the *_values variants instead (_native.pyx:248-350): `out` f64 [rows, cols] gets the
+ *   dequantized values (codes / scales unused; QuEST still writes mask).
+ * qt_seam_fwht: in-place blockwise FWHT of x [rows, n] (f64 != 0: double, else float), block g a power of
+ *   two dividing n (_native.pyx:353-379).
+ * qt_seam_gemm_nt: c [m, n] = a [m, k] b [n, k]^T, each output summed c = c + a*b over ascending k from zero
+ *   (_native.pyx:382-396), f32 or f64.
+ * qt_seam_row_sums: out[r] = numpy add.reduce of row r of e = (a - b)^2 (op 0) or a * b (op 1) -- numpy's
+ *   pairwise order, so the results equal the reference's ((x - d) ** 2).mean(axis=1) * n and
+ *   (y * qy).sum(axis=1) bit for bit (diagnostics.py:84, 161-165). */
+QT_API int qt_seam_quantize(const double* x, int64_t rows, int64_t cols, int64_t group, int rounding, int values,
+                            uint64_t seed, uint64_t counter_start, double ratio_lo, uint8_t* codes, uint8_t* scales,
+                            uint8_t* mask, double* out, void* stream);
+QT_API int qt_seam_fwht(void* x, int f64, int64_t rows, int64_t n, int64_t g, void* stream);
+QT_API int qt_seam_gemm_nt(const void* a, const void* b, void* c, int f64, int64_t m, int64_t n, int64_t k,
+                           void* stream);
+QT_API int qt_seam_row_sums(const double* a, const double* b, int op, int64_t rows, int64_t n, double* out,
+                            void* stream);
+
 /* ---- Llama-loop glue (not on the Quartet path; llama.py): fused bf16 elementwise kernels, fp32 math.
  * qt_rope: half-split rotary embedding of x [batch, seq, heads, head_dim] (rows = batch * seq; element
  *   strides stride_b / stride_s / stride_h, head_dim contiguous) with cos/sin tables [seq, head_dim], into a

@@ -9,7 +9,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_build", "libquartet_b200.so")
+# QT_LIB_PATH: load another build of the library (A/B experiments with tools/; never set in production)
+LIB_PATH = os.environ.get("QT_LIB_PATH") or os.path.join(HERE, "_build", "libquartet_b200.so")
 
 QT_IN_BF16, QT_IN_F32, QT_IN_MXFP4 = 0, 1, 2
 QT_TRANSFORM_NONE, QT_TRANSFORM_HADAMARD, QT_TRANSFORM_RANDOMIZED = 0, 1, 2
@@ -39,6 +40,11 @@ SIGNATURES = {
     "qt_swiglu": (_i32, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp]),
     "qt_cross_entropy": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _f32, _i32, _vp]),
     "qt_rmsnorm": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _f32, _i32, _vp]),
+    "qt_seam_quantize": (_i32, [_vp, _i64, _i64, _i64, _i32, _i32, _u64, _u64, ctypes.c_double, _vp, _vp, _vp, _vp,
+                                _vp]),
+    "qt_seam_fwht": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp]),
+    "qt_seam_gemm_nt": (_i32, [_vp, _vp, _vp, _i32, _i64, _i64, _i64, _vp]),
+    "qt_seam_row_sums": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _vp]),
     "qt_fwht32": (_i32, [_vp, _vp, _i64, _i64, _i32, _vp, _f32, _vp]),
     "qt_quant_rows": (_i32, [_vp, _i32, _i64, _i64, _i64, _i32, _vp, _f32, _i32, _u64, _u64, _i64,
                              _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp]),

@@ -98,6 +98,36 @@ int qt_sign_bits_pair(uint32_t* a, int64_t start_a, int64_t n_a, uint32_t* b, in
     return launch_signs2(a, start_a, n_a, b, start_b, n_b, xi, (cudaStream_t)stream);
 }
 
+// ---- exact plugin seam (seam.cu): f64 / any-group replays of _native.pyx:104-396
+int qt_seam_quantize(const double* x, int64_t rows, int64_t cols, int64_t group, int rounding, int values,
+                     uint64_t seed, uint64_t counter_start, double ratio_lo, uint8_t* codes, uint8_t* scales,
+                     uint8_t* mask, double* out, void* stream) {
+    if (rows < 0 || cols < 0 || group < 1) return QT_ERR_SHAPE;
+    if (rounding < 0 || rounding > 2) return QT_ERR_ARG;
+    if (rows == 0 || cols == 0) return 0;
+    if (!x || (values ? !out : (!codes || !scales)) || (rounding == QT_ROUND_QUEST && !mask)) return QT_ERR_ARG;
+    return launch_seam_quant(x, rows, cols, group, rounding, values != 0, seed, counter_start, ratio_lo, codes,
+                             scales, mask, out, (cudaStream_t)stream);
+}
+
+int qt_seam_fwht(void* x, int f64, int64_t rows, int64_t n, int64_t g, void* stream) {
+    if (rows < 0 || n < 0 || g < 1 || (g & (g - 1)) != 0 || n % g != 0) return QT_ERR_SHAPE;
+    if (rows == 0 || n == 0) return 0;
+    return launch_seam_fwht(x, f64 != 0, rows, n, g, (cudaStream_t)stream);
+}
+
+int qt_seam_gemm_nt(const void* a, const void* b, void* c, int f64, int64_t m, int64_t n, int64_t k, void* stream) {
+    if (m < 0 || n < 0 || k < 0) return QT_ERR_SHAPE;
+    return launch_seam_gemm_nt(a, b, c, f64 != 0, m, n, k, (cudaStream_t)stream);
+}
+
+int qt_seam_row_sums(const double* a, const double* b, int op, int64_t rows, int64_t n, double* out, void* stream) {
+    if (rows < 0 || n < 0) return QT_ERR_SHAPE;
+    if (op != 0 && op != 1) return QT_ERR_ARG;
+    if (op == 0 && !b && rows > 0 && n > 0) return QT_ERR_ARG;
+    return launch_seam_row_sums(a, op == 1 && !b ? a : b, op, rows, n, out, (cudaStream_t)stream);
+}
+
 int qt_fwht32(const float* x, float* out, int64_t rows, int64_t cols, int transform, const uint32_t* sign_bits,
              float prescale, void* stream) {
     if (cols % 32 != 0 || rows < 0) return QT_ERR_SHAPE;

@@ -45,25 +45,6 @@ __device__ __forceinline__ float exp2i(int e) {  // 2^e as fp32, e in [-149, 127
     return __uint_as_float(1u << (e + 149));
 }
 
-// Blockwise orthonormal FWHT on 32 register values, replaying _native.pyx:366-378 exactly:
-// stages h = 1, 2, 4, 8, 16; (a + b) * c and (a - b) * c with the lower index as minuend;
-// c = fp32(1/sqrt(2)); every op rounded separately (the _rn intrinsics are never contracted).
-__device__ __forceinline__ void fwht32(float (&v)[32]) {
-    const float c = 0.70710678118654752440f;  // 0x3F3504F3 == (float)(1.0 / sqrt(2.0))
-#pragma unroll
-    for (int h = 1; h < 32; h *= 2) {
-#pragma unroll
-        for (int s = 0; s < 32; s += 2 * h) {
-#pragma unroll
-            for (int t = s; t < s + h; ++t) {
-                float a = v[t], b = v[t + h];
-                v[t] = __fmul_rn(__fadd_rn(a, b), c);
-                v[t + h] = __fmul_rn(__fsub_rn(a, b), c);
-            }
-        }
-    }
-}
-
 // E2M1 encode of two fp32 values with RNE + satfinite (ties-to-even-mantissa, clamp at 6):
 // identical to the reference's midpoint ladder (_numpy.py:26-40).  Returns the byte with `lo`
 // in the low nibble.  Negative zero is NOT canonicalised here (see canon_nz).
@@ -122,8 +103,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Wait for the phase with the given parity.  QT_WAIT_HINT (build flag, default 0): 0 = plain try_wait
+// loop (the hardware parks the warp inside SYNCS.TRYWAIT until the phase completes or a short timeout),
+// 1 = try_wait with a suspend-time hint, which ptxas turns into a NANOSLEEP.SYNCS retry loop.
+#ifndef QT_WAIT_HINT
+#define QT_WAIT_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t addr = smem_u32(bar);
+#if QT_WAIT_HINT
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
@@ -135,12 +123,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "}\n" ::"r"(addr),
         "r"(parity)
         : "memory");
+#else
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(addr),
+        "r"(parity)
+        : "memory");
+#endif
 }
 
-// Same with a bounded suspend hint (ns) per try: a waiting warp sleeps inside try_wait instead of
-// re-issuing, so long waits do not steal issue slots from working warps of the same SMSP.
 template <int HINT_NS>
 __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity) {
+#if QT_WAIT_HINT
     uint32_t addr = smem_u32(bar);
     asm volatile(
         "{\n"
@@ -153,6 +153,9 @@ __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity) {
         "}\n" ::"r"(addr),
         "r"(parity), "n"(HINT_NS)
         : "memory");
+#else
+    mbar_wait(bar, parity);
+#endif
 }
 
 // one lane of the (fully active) warp: for issuing single-thread async ops from warp-uniform code

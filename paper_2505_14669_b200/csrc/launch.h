@@ -82,4 +82,14 @@ int launch_gemm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, int64_t a_ka
                 const uint8_t* b_sf, int64_t b_katoms, int64_t M, int64_t N, int64_t K, const EpiParams& ep,
                 cudaStream_t st);
 
+// seam.cu: exact scalar replays of the reference's kernels for f64 / any-group inputs
+int launch_seam_quant(const double* x, int64_t rows, int64_t cols, int64_t group, int rounding, bool values,
+                      uint64_t seed, uint64_t counter_start, double ratio_lo, uint8_t* codes, uint8_t* scales,
+                      uint8_t* mask, double* out, cudaStream_t st);
+int launch_seam_fwht(void* x, bool f64, int64_t rows, int64_t n, int64_t g, cudaStream_t st);
+int launch_seam_gemm_nt(const void* a, const void* b, void* c, bool f64, int64_t m, int64_t n, int64_t k,
+                        cudaStream_t st);
+int launch_seam_row_sums(const double* a, const double* b, int op, int64_t rows, int64_t n, double* out,
+                         cudaStream_t st);
+
 }  // namespace qt

@@ -42,7 +42,8 @@ struct XqArgs {
     QuantOut col_out;         // X_t [C, R]
     float col_prescale;
     int* fallbacks;           // re-decided groups (nullable): [0] X_q search, [1] X_t, [2] X_q codes only
-    int dbg;                  // experiment knobs (0 in production)
+    int dbg;                  // experiment knobs (0 in production): 1 skip QuEST decisions, 2 skip RTN decisions,
+                              // 4 exact CUDA-core row phase for every group
 };
 
 constexpr float kU24 = 5.9604645e-08f;  // 2^-24
@@ -370,7 +371,9 @@ __global__ void __launch_bounds__(kXqThreads, 1) k_tcq_xq(const __grid_constant_
                 const bool valid = row < a.R && gg * 32 < a.C;
                 const uint8_t* tile = smem + s * kXqIn;
                 int st = 0;
-                if (a.dbg & 1) {  // experiment: skip the QuEST decisions (timing only)
+                if (a.dbg & 4) {  // experiment: every row group on the exact CUDA-core path (hybrid timing)
+                    st = 1;
+                } else if (a.dbg & 1) {  // experiment: skip the QuEST decisions (timing only)
                     codes = make_uint4(__float_as_uint(acc[0]), __float_as_uint(acc[9]), __float_as_uint(acc[17]),
                                        __float_as_uint(acc[31]));
                     e = 120;

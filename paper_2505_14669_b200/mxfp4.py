@@ -253,7 +253,17 @@ def gemm(a: MXOperand, b: MXOperand, *, out_dtype=torch.float32, mask: torch.Ten
     if accumulate and (out is None or tuple(out.shape) != (M, N)):
         raise ValueError("accumulate=True needs an [M, N] out tensor")
     if out is None:
+        if out_dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError(f"gemm output dtype must be bfloat16 or float32, got {out_dtype}")
         out = torch.empty((M, N), dtype=out_dtype, device=a.codes.device)
+    else:
+        if out.dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError(f"gemm output dtype must be bfloat16 or float32, got {out.dtype}")
+        if out.dim() != 2 or tuple(out.shape) != (M, N) or out.stride(1) != 1 or out.stride(0) < N:
+            raise ValueError(f"gemm out must be a row-major [{M}, {N}] view with unit column stride, got "
+                             f"shape {tuple(out.shape)} strides {tuple(out.stride())}")
+        if out.device != a.codes.device:
+            raise ValueError(f"gemm out is on {out.device}, operands on {a.codes.device}")
     odt = _lib.QT_OUT_BF16 if out.dtype == torch.bfloat16 else _lib.QT_OUT_F32
     epi = _lib.QT_EPI_STORE if mask is None else (_lib.QT_EPI_MASK_H if hadamard else _lib.QT_EPI_MASK)
     if accumulate:
@@ -263,4 +273,78 @@ def gemm(a: MXOperand, b: MXOperand, *, out_dtype=torch.float32, mask: torch.Ten
                                   mask.data_ptr() if mask is not None else None, float(scale),
                                   _stream(out.device))
     check(rc, "qt_gemm_mxf4")
+    return out
+
+
+# ---- exact plugin seam (qt_seam_*, seam.cu): f64 / any-group replays of _native.pyx:104-396 -------------
+def seam_quantize(x: torch.Tensor, group: int, rounding: int, *, seed: int = 0, counter_start: int = 0,
+                  ratio_lo: float = 1.0 / 16.0, values: bool = False):
+    """quantize_{rtn,sr,quest} (values=False: unpacked codes u8 [R, C], scales u8 [R, ceil(C/g)], QuEST mask)
+    or *_values (values=True: f64 values [R, C], QuEST mask) of a f64 device matrix, bit-identical to the
+    reference's kernels for every input (_native.pyx:104-350)."""
+    _require_cuda(x, "x")
+    if x.dtype != torch.float64 or x.dim() != 2:
+        raise ValueError("seam quantizers take a 2-D float64 matrix")
+    x = x.contiguous()
+    rows, cols = x.shape
+    ng = -(-cols // group) if group > 0 else 0
+    dev = x.device
+    quest = rounding == _lib.QT_ROUND_QUEST
+    mask = torch.empty((rows, cols), dtype=torch.uint8, device=dev) if quest else None
+    if values:
+        out = torch.empty((rows, cols), dtype=torch.float64, device=dev)
+        codes = scales = None
+    else:
+        out = None
+        codes = torch.empty((rows, cols), dtype=torch.uint8, device=dev)
+        scales = torch.empty((rows, ng), dtype=torch.uint8, device=dev)
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    rc = _lib.load().qt_seam_quantize(x.data_ptr(), rows, cols, int(group), int(rounding), int(values),
+                                      int(seed) & 0xFFFFFFFFFFFFFFFF, int(counter_start) & 0xFFFFFFFFFFFFFFFF,
+                                      float(ratio_lo), ptr(codes), ptr(scales), ptr(mask), ptr(out), _stream(dev))
+    check(rc, "qt_seam_quantize")
+    if values:
+        return (out, mask) if quest else out
+    return (codes, scales, mask) if quest else (codes, scales)
+
+
+def seam_fwht(x: torch.Tensor, g: int) -> torch.Tensor:
+    """Blockwise FWHT of a f32 / f64 device matrix along its rows, any power-of-two block g
+    (_native.pyx:353-379), on a copy."""
+    _require_cuda(x, "x")
+    if x.dtype not in (torch.float32, torch.float64) or x.dim() != 2:
+        raise ValueError("seam fwht takes a 2-D float32 / float64 matrix")
+    out = x.contiguous().clone()
+    rc = _lib.load().qt_seam_fwht(out.data_ptr(), int(out.dtype == torch.float64), out.shape[0], out.shape[1],
+                                  int(g), _stream(out.device))
+    check(rc, "qt_seam_fwht")
+    return out
+
+
+def seam_gemm_nt(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """a @ b.T with the reference's fixed ascending-k order per output (_native.pyx:382-396), f32 or f64."""
+    _require_cuda(a, "a")
+    if a.dtype != b.dtype or a.dtype not in (torch.float32, torch.float64):
+        raise ValueError("seam gemm_nt takes two float32 or two float64 matrices")
+    a, b = a.contiguous(), b.contiguous()
+    m, k = a.shape
+    n = b.shape[0]
+    c = torch.empty((m, n), dtype=a.dtype, device=a.device)
+    rc = _lib.load().qt_seam_gemm_nt(a.data_ptr(), b.data_ptr(), c.data_ptr(), int(a.dtype == torch.float64), m, n,
+                                     k, _stream(a.device))
+    check(rc, "qt_seam_gemm_nt")
+    return c
+
+
+def seam_row_sums(a: torch.Tensor, b: torch.Tensor | None, op: int) -> torch.Tensor:
+    """numpy's add.reduce along rows of (a - b)^2 (op 0) or a * b (op 1; b None = a), pairwise order."""
+    _require_cuda(a, "a")
+    a = a.contiguous()
+    if b is not None:
+        b = b.contiguous()
+    rows, n = a.shape
+    out = torch.empty(rows, dtype=torch.float64, device=a.device)
+    rc = _lib.load().qt_seam_row_sums(a.data_ptr(), b.data_ptr() if b is not None else None, int(op), rows, n,
+                                      out.data_ptr(), _stream(a.device))
+    check(rc, "qt_seam_row_sums")
     return out

@@ -181,6 +181,7 @@ def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, polic
     then also produces the transposed backward operands X_t and W_t (qt_quant_fused), which backward
     reuses instead of re-reading X_q / W_q.  Results are identical either way."""
     _check_policy(policy, scheme)
+    _check_out_dtype("out_dtype", out_dtype)
     if x.dim() != 2 or w.dim() != 2:
         raise ValueError("x and w must be 2-D")
     batch, d_in = x.shape
@@ -236,6 +237,12 @@ def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, polic
     return y, ctx
 
 
+def _check_out_dtype(name: str, dt: torch.dtype) -> None:
+    """The GEMM epilogues store bf16 or fp32 only; reject anything else before any device work."""
+    if dt not in (torch.float32, torch.bfloat16):
+        raise ValueError(f"{name} must be torch.float32 or torch.bfloat16, got {dt}")
+
+
 def _rounding_code(rounding: str) -> int:
     if rounding == "rtn":
         return _lib.QT_ROUND_RTN
@@ -261,10 +268,18 @@ def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn"
     along the token axis are then the global ones, so its G / G_t / X_t operands are exactly the
     corresponding slices of the single-GPU operands, its dx rows are exactly the single-GPU dx rows,
     and the sum of the ranks' dw equals the single-GPU dw up to fp32 summation order (the masked
-    Hadamard epilogue is linear).  token_offset must be a multiple of 32."""
+    Hadamard epilogue is linear).  token_offset must be a multiple of 32.
+
+    Restriction vs the reference: d_out and batch must be multiples of the block size even with
+    hadamard=False (the reference checks them only for hadamard=True and quantizes a ragged trailing
+    group).  They are the contraction axes of the dx / dw GEMMs, whose MXFP4 operands are whole
+    32-element blocks; ragged shapes raise ValueError here (INTEGRATION.md lists the rejected cases)."""
     if rounding not in ("exact", "rtn", "sr"):
         raise ValueError(f"unknown backward rounding {rounding!r}")
     rc = _rounding_code(rounding)
+    _check_out_dtype("dw_dtype", dw_dtype)
+    if dx_accumulate is None:
+        _check_out_dtype("dx_dtype", dx_dtype)
     if tuple(dy.shape) != (ctx.batch, ctx.d_out):
         raise ValueError(f"dy shape {tuple(dy.shape)}, expected {(ctx.batch, ctx.d_out)}")
     g = ctx.scheme.group_size

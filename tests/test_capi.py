@@ -82,3 +82,23 @@ def test_empty_dimensions_are_no_ops(lib):
     assert lib.qt_gemm_mxf4(None, None, None, None, 0, 32, 64, None, 0, 32, 1, None, 1.0, None) == 0   # M = 0
     assert lib.qt_gemm_mxf4(None, None, None, None, 32, 32, 0, None, 0, 32, 0x11, None, 1.0, None) == 0  # D += 0
     assert lib.qt_gemm_mxf4(None, None, None, None, -32, 32, 64, None, 0, 32, 0, None, 1.0, None) == 2001
+
+
+def test_layer_rejects_unsupported_output_dtypes():
+    """The GEMM epilogues store bf16 / fp32 only: other dtypes raise before any device work (no
+    out-of-bounds write into a 2-byte fp16 buffer)."""
+    import torch
+
+    import paper_2505_14669_b200 as qt
+
+    x = torch.zeros(32, 32)
+    with pytest.raises(ValueError, match="out_dtype"):
+        qt.forward(x, x, out_dtype=torch.float16)
+    with pytest.raises(ValueError, match="out_dtype"):
+        qt.forward(x, x, out_dtype=torch.float64)
+    ctx = qt.LayerContext(x_q=None, w_q=None, scheme=qt.QUEST, policy=qt.DEFAULT_POLICY, hadamard=True, batch=32,
+                          d_in=32, d_out=32)
+    with pytest.raises(ValueError, match="dx_dtype"):
+        qt.backward(x, ctx, xi=1, dx_dtype=torch.float16)
+    with pytest.raises(ValueError, match="dw_dtype"):
+        qt.backward(x, ctx, xi=1, dw_dtype=torch.float16)

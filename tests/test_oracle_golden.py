@@ -99,3 +99,11 @@ def test_golden_mxf4_container(oracle, golden_dir):
     blob = oracle.serialize(c, s)
     with open(os.path.join(golden_dir, "golden.mxf4"), "rb") as f:
         assert blob == f.read()
+
+
+def test_diagnostics_gaussian_stream_matches_reference(golden_dir):
+    """The host sample stream of the GPU diagnostics is rng.gaussians itself (rng.py:65-69)."""
+    from paper_2505_14669_b200 import diagnostics
+
+    g = _load(golden_dir, "rng.npz")["gauss"]
+    assert np.array_equal(diagnostics.gaussians(1, 0x4755, 0, 1000), g)

@@ -18,9 +18,15 @@ def t(f, n=10):
     b.record(); torch.cuda.synchronize()
     return a.elapsed_time(b) * 1000 / n
 fb = torch.zeros(3, dtype=torch.int32, device="cuda")
-for mode, name in ((3, "tc full (QuEST+RTN)"), (3 | 1 << 4, "tc full, no QuEST"), (3 | 2 << 4, "tc full, no col RTN"), (3 | 3 << 4, "tc full, skeleton"), (0, "cuda-core fused")):
+f = lambda: quant_fused(x, Q, RTN, transform=H, col_transform=RT, col_signs=s)  # noqa: E731
+for mode, name in ((3, "tc full (QuEST+RTN)"), (3 | 4 << 4, "hybrid: exact rows"), (3 | 1 << 4, "tc full, no QuEST"),
+                   (3 | 2 << 4, "tc full, no col RTN"), (3 | 3 << 4, "tc full, skeleton"), (0, "cuda-core fused")):
+    L.qt_debug_set_quant(mode, None)
+    us = t(f)
     fb.zero_()
     L.qt_debug_set_quant(mode, fb.data_ptr())
-    print(f"{name:22s} {t(lambda: quant_fused(x, Q, RTN, transform=H, col_transform=RT, col_signs=s)):8.1f} us  fallbacks {fb.tolist()}")
+    f()
+    torch.cuda.synchronize()
+    print(f"{name:22s} {us:8.1f} us  fallbacks {fb.tolist()}", flush=True)
 L.qt_debug_set_quant(0, None)
 print(f"{'rows only (k_quant)':22s} {t(lambda: quant_rows(x, H, Q, want_mask=True)):8.1f} us")
