@@ -324,17 +324,27 @@ def run_ours(args, rank, world, local_rank):
         dy = torch.randn(T, d_out, device=dev, generator=g).to(torch.bfloat16)
         data.append((x, w, dy))
 
-    def step(xi):
+    def shape_step(i, xi, rounding="rtn"):
+        x, w, dy = data[i]
+        # the step's backward seed is known at forward time (train.py:346-348), so X_t / W_t come
+        # out of the forward read of X / W (qt_quant_fused)
+        # rank r holds tokens [r T, (r + 1) T) of the global batch: global sign / SR offsets make its
+        # operands exact slices of the single-GPU operands (dp.py)
+        y, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False, bwd_xi=xi * 3 + i,
+                            bwd_rounding=rounding, token_offset=rank * T, total_tokens=world * T)
+        dx, dw = qt.backward(dy, ctx, xi=xi * 3 + i, rounding=rounding, dx_dtype=torch.bfloat16,
+                             dw_dtype=torch.float32, check_finite=False, token_offset=rank * T,
+                             total_tokens=world * T)
+        return dw
+
+    def step(xi, rounding="rtn", graphs=None):
         pending = []
-        for i, (x, w, dy) in enumerate(data):
-            # the step's backward seed is known at forward time (train.py:346-348), so X_t / W_t come
-            # out of the forward read of X / W (qt_quant_fused)
-            # rank r holds tokens [r T, (r + 1) T) of the global batch: global sign / SR offsets make its
-            # operands exact slices of the single-GPU operands (dp.py)
-            y, ctx = qt.forward(x, w, out_dtype=torch.bfloat16, check_finite=False, bwd_xi=xi * 3 + i,
-                                token_offset=rank * T, total_tokens=world * T)
-            dx, dw = qt.backward(dy, ctx, xi=xi * 3 + i, dx_dtype=torch.bfloat16, dw_dtype=torch.float32,
-                                 check_finite=False, token_offset=rank * T, total_tokens=world * T)
+        for i in range(len(data)):
+            if graphs is not None:
+                graphs[i][0].replay()
+                dw = graphs[i][1]
+            else:
+                dw = shape_step(i, xi, rounding)
             if world > 1:  # data parallel: the token-sum of dW is the only exchange (bf16, NCCL); it runs
                 # asynchronously on NCCL's stream while the next shape computes, and is waited for at step end
                 buf = dw.to(torch.bfloat16)
@@ -343,25 +353,35 @@ def run_ours(args, rank, world, local_rank):
             work.wait()
             dw.copy_(buf)
 
-    for i in range(args.warmup):
-        step(i)
-    torch.cuda.synchronize()
-    graph = None
-    # world > 1: the step contains NCCL all-reduces; they are launched eagerly rather than captured
-    if not args.no_graph and world == 1:
-        # capture one full step (all shapes, fwd + bwd) once; every replay re-executes every kernel
-        graph = torch.cuda.CUDAGraph()
+    def capture(fn):
+        g_ = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
         cap.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(cap):
-            step(args.warmup)
+            fn()
             torch.cuda.synchronize()
-            with torch.cuda.graph(graph, stream=cap):
-                step(args.warmup + 1)
+            with torch.cuda.graph(g_, stream=cap):
+                out = fn()
         torch.cuda.current_stream().wait_stream(cap)
-        for _ in range(2):
+        return g_, out
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    graph = graphs = None
+    if not args.no_graph and world == 1:
+        # capture one full step (all shapes, fwd + bwd) once; every replay re-executes every kernel
+        graph, _ = capture(lambda: step(args.warmup + 1))
+    elif not args.no_graph:
+        # N > 1: each shape's compute is one captured graph (the same kernels as the N = 1 graph); the
+        # bf16 dW all-reduces are launched between the replays so they overlap the next shape's compute
+        graphs = [capture(lambda i=i: shape_step(i, args.warmup + 1)) for i in range(len(data))]
+    for _ in range(2):
+        if graph is not None:
             graph.replay()
-        torch.cuda.synchronize()
+        else:
+            step(args.warmup, graphs=graphs)
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     sampler = ClockSampler(local_rank) if rank == 0 and not args.no_clocks else None
@@ -376,7 +396,7 @@ def run_ours(args, rank, world, local_rank):
         if graph is not None:
             graph.replay()
         else:
-            step(args.warmup + i)
+            step(args.warmup + i, graphs=graphs)
     end.record()
     torch.cuda.synchronize()
     clocks = sampler.stop() if sampler else None
@@ -387,6 +407,23 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    # the same step with stochastic-rounding backward operands (qlinear.py:168-175, rounding="sr"): the SR
+    # quantizers run on the CUDA cores (the tensor-core dual quantizer is RTN-only)
+    sr = None
+    if world == 1 and not args.no_graph:
+        g_sr, _ = capture(lambda: step(args.warmup + 2, rounding="sr"))
+        g_sr.replay()
+        torch.cuda.synchronize()
+        s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(args.steps):
+            g_sr.replay()
+        e0.record()
+        torch.cuda.synchronize()
+        sr_ms = s0.elapsed_time(e0) / args.steps
+        sr = {"value": round(flops_per_step(T) / (sr_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+              "ms_per_step": round(sr_ms, 4), "what": "same step, backward rounding 'sr' (G, G_t, W_t, X_t by SR)"}
+        del g_sr
     # end to end at N GPUs: every rank streams its own shard through its own PCIe link; max over ranks
     if world > 1:
         dist.barrier()
@@ -442,7 +479,9 @@ def run_ours(args, rank, world, local_rank):
                    "shapes_din_dout": SHAPES, "tokens_per_gpu": T, "global_tokens": T * world,
                    "scheme": "quest fwd / rtn bwd, hadamard g=32", "parallelism": f"dp{world}",
                    "l2": "inputs larger than L2 (x/dy 128-344 MB per shape); no flush needed",
-                   "launch": "CUDA graph replay of one captured step" if graph is not None else "eager"},
+                   "launch": ("CUDA graph replay of one captured step" if graph is not None else
+                              "one CUDA graph per shape, bf16 dW NCCL all-reduces launched between replays"
+                              if graphs is not None else "eager")},
         "tokens_per_s": round(world * T * len(SHAPES) / (ms * 1e-3), 1),
         "bf16_cublas": {"value": round(flops_per_step(T) / (bf16_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
                         "ms_per_step": round(bf16_ms, 4), "speedup_ours": round(bf16_ms / ms, 3),
@@ -460,6 +499,7 @@ def run_ours(args, rank, world, local_rank):
                                "unit": "GB/s", "frac": round(q_gbs / peaks["hbm_gbs"], 4),
                                "share_of_step": round(q_us * 1e-3 / ms, 4)},
         "kernels": table,
+        "sr_backward": sr,
         "e2e": e2e,
         # per step and shape: 2 sign bitmaps + 2 fused forward quantizers + 1 GEMM; 1 dual quantizer + 2 GEMMs
         "gpu_launches": 7 * len(SHAPES) * args.steps,  # signs pair, fused X, fused W, GEMM, dual dy, 2 GEMMs

@@ -103,29 +103,28 @@ static __device__ __noinline__ int quest_exact_cold(const float* xs, int e_hi, i
 // Stochastic rounding of one element (_native.pyx:156-167): v = x / s in f64, neighbours on the
 // signed grid, p = (v - lo) / (hi - lo) in f64, u = splitmix64 uniform at `index`, hi when u < p.
 __device__ __forceinline__ uint32_t sr_code(float x, float sc_f, double sc_d, uint64_t base, uint64_t index) {
-    float a = fabsf(x) * sc_f;
+    const float a = fabsf(x) * sc_f;
     int b;
-    double lo, hi;
+    double lo;
     uint32_t c_lo, c_hi;
     if (x > 0.0f) {
         b = (a > 0.5f) + (a > 1.0f) + (a > 1.5f) + (a > 2.0f) + (a > 3.0f) + (a > 4.0f);
-        lo = b <= 4 ? 0.5 * b : (double)(b - 2);
-        hi = b + 1 <= 4 ? 0.5 * (b + 1) : (b + 1 == 7 ? 6.0 : (double)(b - 1));
+        lo = b <= 4 ? 0.5 * b : (double)(b - 2);                              // grid(b)
         c_lo = (uint32_t)b;
         c_hi = (uint32_t)(b + 1);
     } else {
         b = (a >= 0.5f) + (a >= 1.0f) + (a >= 1.5f) + (a >= 2.0f) + (a >= 3.0f) + (a >= 4.0f);
-        double plo = b <= 4 ? 0.5 * b : (double)(b - 2);
-        double phi = b + 1 <= 4 ? 0.5 * (b + 1) : (b + 1 == 7 ? 6.0 : (double)(b - 1));
-        lo = -phi;
-        hi = -plo;
+        lo = -(b + 1 <= 4 ? 0.5 * (b + 1) : (b + 1 == 7 ? 6.0 : (double)(b - 1)));   // -grid(b + 1)
         c_lo = 8u | (uint32_t)(b + 1);
         c_hi = b == 0 ? 0u : (8u | (uint32_t)b);
     }
-    double v = (double)x * sc_d;
-    double p = __dmul_rn(__dsub_rn(v, lo), 1.0 / (hi - lo));  // span is a power of two: exact
-    uint64_t h = mix64(base + (index + 1) * kGolden);
-    double u = (double)(h >> 11) * (1.0 / 9007199254740992.0);
+    const double v = (double)x * sc_d;
+    // the span hi - lo is 0.5 (b < 4), 1 (b = 4, 5) or 2 (b = 6): dividing by it equals multiplying by the
+    // exact reciprocal (both are the correctly rounded value of the same real), with no double division
+    const double inv_span = b < 4 ? 2.0 : (b < 6 ? 1.0 : 0.5);
+    const double p = __dmul_rn(__dsub_rn(v, lo), inv_span);
+    const uint64_t h = mix64(base + (index + 1) * kGolden);
+    const double u = (double)(h >> 11) * (1.0 / 9007199254740992.0);
     return u < p ? c_hi : c_lo;
 }
 

@@ -218,18 +218,36 @@ __global__ void __launch_bounds__(kTqThreads, 1)
                 const QuantOut& out = pass ? a.col_out : a.row_out;
                 const int64_t orow = pass ? c0 + li : r0 + li;           // output row
                 const int64_t kb = pass ? r0 : c0;                      // start of the grouped axis (mult. of 128)
-                if (orow < (pass ? a.C : a.R)) {
-                    const int64_t lim_k = pass ? a.R : a.C;
-                    if (!ok0 || !ok1) {
-                        const uint32_t* sg = pass ? a.sign_r : a.sign_c;
-                        for (int u = 0; u < 2; ++u) {
-                            const int64_t gk = kb + 32 * (g0 + u);
-                            if ((u ? ok1 : ok0) || gk >= lim_k) continue;
-                            if (a.fallbacks) atomicAdd(a.fallbacks, 1);
-                            exact_group(tile, pass == 1, li, g0 + u, __ldg(sg + (gk >> 5)), a.prescale, out.err,
-                                        u ? c1d : c0d, u ? e1 : e0);
+                const int64_t lim_k = pass ? a.R : a.C;
+                const bool in_row = orow < (pass ? a.C : a.R);
+                // undecided groups (~0.1 %): the whole warp recomputes them exactly, one group at a time
+                {
+                    const uint32_t* sg = pass ? a.sign_r : a.sign_c;
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int64_t gk = kb + 32 * (g0 + u);
+                        uint32_t todo = __ballot_sync(0xffffffffu, in_row && !(u ? ok1 : ok0) && gk < lim_k);
+                        if (todo && a.fallbacks && lane == 0) atomicAdd(a.fallbacks, __popc(todo));
+                        const uint32_t sw = todo && gk < lim_k ? __ldg(sg + (gk >> 5)) : 0u;
+                        while (todo) {
+                            const int f = __ffs(todo) - 1;
+                            todo &= todo - 1;
+                            uint4 cx;
+                            int ex;
+                            exact_group_warp(tile, pass == 1, quad * 32 + f, g0 + u, sw, a.prescale, out.err, cx, ex);
+                            if (lane == f) {
+                                if (u) {
+                                    c1d = cx;
+                                    e1 = ex;
+                                } else {
+                                    c0d = cx;
+                                    e0 = ex;
+                                }
+                            }
                         }
                     }
+                }
+                if (in_row) {
                     uint8_t* cp = out.codes + orow * out.ldc + (kb >> 5) * 16 + g0 * 16;
                     // scale atom bytes of groups g0, g0 + 1 are adjacent: ((r/128) katoms + k/128) * 512 +
                     // (r % 32) * 16 + ((r / 32) % 4) * 4 + g

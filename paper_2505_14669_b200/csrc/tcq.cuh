@@ -40,7 +40,9 @@ __device__ __forceinline__ bool rtn_checked(const float (&acc)[32], float presca
     const float amax = absmax32(acc);
     // branch-free so that two groups interleave; acc == 0 only for x == 0 (H is invertible and the error
     // is below |Hx|), which encodes to zero codes with e = 0 like the reference
-    bool ok = amax <= 1.0e30f && (amax >= 1.0e-30f || amax == 0.0f);   // NaN / huge / subnormal -> exact
+    // NaN / huge / tiny -> exact.  Below 1e-25 a subnormal bf16 operand the tensor core may flush (<= 32 * 2^-126
+    // in all) would no longer sit far below the bound
+    bool ok = amax <= 1.0e30f && (amax >= 1.0e-25f || amax == 0.0f);
 #if QT_RTN_L2
     // sum|x| <= ||H x||_2: one FFMA per element buys a ~2.5x tighter bound than sqrt(32) max|H x|
     float ss0 = 0.f, ss1 = 0.f;
@@ -103,6 +105,42 @@ static __device__ __noinline__ void exact_group(const uint8_t* tile, bool col, i
     cf.prescale = prescale;
     uint32_t mask;
     e_out = quant_group<kRtn>(v, cf, 0, err, nullptr, codes, mask);
+}
+
+// Warp-cooperative version of exact_group for ONE group (all 32 lanes; lane j holds element j): the checked
+// epilogues hand their rare undecided groups to this one at a time instead of running exact_group in a single
+// diverged lane.  Same operations as the scalar path: the butterfly pairs (t, t + h) meet through a shuffle,
+// the lower index stays the minuend; max |v| is order-independent; each lane encodes its own element.
+__device__ __forceinline__ float max_nan2(float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void exact_group_warp(const uint8_t* tile, bool col, int idx, int g, uint32_t sw,
+                                                 float prescale, int* err, uint4& codes, int& e_out) {
+    const int j = threadIdx.x & 31;
+    const int r = col ? g * 32 + j : idx, c = col ? idx : g * 32 + j;
+    const uint16_t h16 = *reinterpret_cast<const uint16_t*>(tile + tq_off(r, c));
+    float v = __uint_as_float(((uint32_t)h16 << 16) ^ (((sw >> j) & 1u) << 31));
+#pragma unroll
+    for (int h = 1; h < 32; h <<= 1) {
+        const float o = __shfl_xor_sync(0xffffffffu, v, h);
+        v = __fmul_rn((j & h) ? __fsub_rn(o, v) : __fadd_rn(v, o), kHc);
+    }
+    float am = fabsf(v);
+#pragma unroll
+    for (int h = 1; h < 32; h <<= 1) am = max_nan2(am, __shfl_xor_sync(0xffffffffu, am, h));
+    if (!(am <= 3.4028234663852886e38f) && err && j == 0) atomicOr(err, 1);
+    int e;
+    float sc;
+    if (!rtn_scale(am, prescale, e, sc)) v = __fmul_rn(v, prescale);
+    uint32_t nib = e2m1b(__fmul_rn(v, sc), 0.0f) & 0xFu;
+    if ((nib & 7u) == 0) nib = 0;   // -0 -> +0 (_native.pyx:127-130)
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[q] = __reduce_or_sync(0xffffffffu, (j >> 3) == q ? nib << (4 * (j & 7)) : 0u);
+    codes = make_uint4(w[0], w[1], w[2], w[3]);
+    e_out = e;
 }
 
 // sign byte -> 8 bf16 +-1.0 (bit i set -> element i negative), 4 KB

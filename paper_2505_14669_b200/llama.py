@@ -276,6 +276,13 @@ class LlamaQuartet(torch.nn.Module):
         self.blocks = torch.nn.ModuleList(Block(cfg, i, seed, device) for i in range(cfg.n_layer))
         self.norm = RMSNorm(cfg.d_model, device=device)
         self.head = None if blocks_only else make_linear(cfg, cfg.d_model, cfg.vocab, seed, 16 * 4096, device)
+        # every linear weight from the model's own generator (N(0, 1/d_in), in registration order): the same
+        # seed gives the same model in every process, which data-parallel ranks rely on
+        with torch.no_grad():
+            for m in self.modules():
+                if isinstance(m, (QuartetLinear, Bf16Linear)):
+                    w = m.weight
+                    w.copy_(torch.randn(w.shape, generator=g).div_(math.sqrt(w.shape[1])).to(w.device, w.dtype))
         cos, sin = _rope(cfg.seq_len, cfg.d_model // cfg.n_head, cfg.rope_base, device)
         self.register_buffer("cos", cos, persistent=False)
         self.register_buffer("sin", sin, persistent=False)
@@ -411,6 +418,12 @@ class Trainer:
                                      fused=params[0].is_cuda)
         self.bucket = OverlappedGradBuckets(params)
         self.step_i = 0
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            with torch.no_grad():   # data parallel: every rank starts from rank 0's weights
+                for p in model.parameters():
+                    dist.broadcast(p.data, src=0)
         self._shard_tokens = None
 
     def _place_shard(self, n_tokens: int) -> None:

@@ -374,3 +374,4 @@ def test_sign_bits_pair_equals_two_calls(qt):
         a, b = sign_bits_pair(12345, n_a, n_b, "cuda", start_b=s_b)
         assert torch.equal(a, sign_bits(12345, n_a, "cuda")) if n_a else a.numel() == 0
         assert torch.equal(b, sign_bits(12345, n_b, "cuda", start=s_b))
+
