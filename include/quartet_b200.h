@@ -188,11 +188,12 @@ QT_API int qt_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_sf, const uint8
  * 1-CTA kernel where the 2-CTA pair kernel is the default, bit 19 runs the pairs in clusters of 8 with TMA
  * multicast of A and B -- both for A/B parity tests). */
 QT_API void qt_debug_set_gemm(int dbg);
-/* Quantizer path selection for A/B parity tests: mode 0 (production) uses the tensor-core Hadamard
- * quantizer for the backward dual operands, mode 1 forces the CUDA-core path everywhere, mode 3 routes
- * the bf16 QuEST forward of qt_quant_fused to the all-tensor-core kernel (checked QuEST + checked RTN,
- * experimental, about par with the CUDA-core kernel); `fallbacks` (nullable device ints: 1 for mode 0,
- * 3 for mode 3) counts groups a tensor-core path re-decided exactly.  Not thread-safe; tests only. */
+/* Quantizer path selection for A/B parity tests: mode 0 (production; 3 is an alias) runs the tensor-core
+ * Hadamard quantizers where they apply -- the backward dual operands (bf16, RTN, randomized) and the bf16 QuEST
+ * forward of qt_quant_fused with an RTN randomized transposed requantization (checked QuEST + checked RTN);
+ * mode 1 forces the CUDA-core kernels everywhere.  `fallbacks` (nullable device ints, 3 of them) counts the
+ * groups a tensor-core path re-decided exactly: [0] dual groups / forward QuEST searches, [1] forward X_t
+ * groups, [2] forward codes-only re-encodes.  Not thread-safe; tests only. */
 QT_API void qt_debug_set_quant(int mode, int* fallbacks);
 /* Parity-test hook: cap every persistent grid (quantizer and GEMM kernels) at max_ctas CTAs (the 2-CTA GEMM
  * at max_ctas/2 pairs, at least one), so that each CTA walks many tiles; 0 restores the production grid.

@@ -10,7 +10,7 @@ static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) 
 static inline uint64_t sr_base_of(uint64_t seed) { return mix64(seed ^ mix64(kDomainSR)); }
 
 static int g_gemm_dbg = 0;  // experiment knobs for qt_debug_set_gemm (never set in production)
-static int g_quant_mode = 0;  // qt_debug_set_quant: 0 production, 1 CUDA cores only, 3 tensor-core QuEST forward
+static int g_quant_mode = 0;  // qt_debug_set_quant: 0 production (tensor-core quantizers where they apply), 1 CUDA cores only
 static int* g_quant_fallbacks = nullptr;
 
 namespace qt {
@@ -231,7 +231,7 @@ int qt_quant_fused(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64
                 col_counter_ld};
     QuantOut ro{row_codes, row_ldc, row_sf, row_katoms, row_mask, err, fallbacks};
     QuantOut co{col_codes, col_ldc, col_sf, col_katoms, nullptr, err, nullptr};
-    if (g_quant_mode == 3 && in_dtype == QT_IN_BF16 && row_rounding == QT_ROUND_QUEST &&
+    if (g_quant_mode != 1 && in_dtype == QT_IN_BF16 && row_rounding == QT_ROUND_QUEST &&
         row_transform == QT_TRANSFORM_HADAMARD && row_prescale == 1.0f && col_rounding == QT_ROUND_RTN &&
         col_transform == QT_TRANSFORM_RANDOMIZED) {
         // X_q and X_t both on the tensor cores (checked QuEST / RTN, exact per-group fallback)

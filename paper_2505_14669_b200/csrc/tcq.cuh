@@ -5,8 +5,8 @@
 #include "qgroup.cuh"
 
 #ifndef QT_RTN_L2
-#define QT_RTN_L2 1  // build flag: 0 = sqrt(32) max|Hx| bound (one FFMA per element less, 4x the exact-path groups:
-                     // measured slower, tools/ab_probe.py)
+#define QT_RTN_L2 0  // build flag: 1 = L2-norm bound in rtn_checked (one FFMA per element more, 1/4 of the exact-path
+                     // groups; with the warp-cooperative fallback the cheaper sqrt(32) max|Hx| bound is 3 % faster)
 #endif
 
 namespace qt {

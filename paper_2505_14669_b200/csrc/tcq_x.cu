@@ -193,54 +193,93 @@ __device__ __forceinline__ uint4 xq_deq8(uint32_t w, float s) {
     return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
-// exact first FWHT stage + tail of tile row r, group g (bf16 SW128 tile) -- the reference's y
-static __device__ __forceinline__ void xq_load_exact(const uint8_t* tile, int r, int g, float (&v)[32]) {
-    const uint8_t* rowp = tile + (g >> 1) * 16384 + r * 128;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const uint4 c = *reinterpret_cast<const uint4*>(rowp + ((((g & 1) * 4 + q) ^ (r & 7)) << 4));
-        const uint32_t w[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const float hi = bf_hi(w[t]);
-            v[q * 8 + 2 * t] = __fmul_rn(fh_add_lo(w[t], hi), kHc);
-            v[q * 8 + 2 * t + 1] = __fmul_rn(fh_sub_lo(w[t], hi), kHc);
-        }
-    }
-    fwht_tail(v);
-}
-
 struct XqGroup {
     uint4 codes;
     uint32_t keep;
     int e;
 };
 
-// status 1: the exact v3 QuEST (search included); status 2: exact codes + mask at the certain exponent e.
-// Results come back by value (registers): reference out-parameters would pin the hot path's codes to the stack.
-static __device__ __noinline__ XqGroup xq_exact_row(const uint8_t* tile, int r, int g, int status, int e, int* err) {
-    float v[32];
-    xq_load_exact(tile, r, g, v);
-    XqGroup o;
-    o.e = e;
-    if (status == 2) {
-        o.codes = encode32_mask(v, exp2i(127 - e), o.keep);
-        return o;
-    }
-    QuantCfg cf{};
-    cf.prescale = 1.0f;
-    o.e = quant_group<kQuest>(v, cf, 0, err, nullptr, o.codes, o.keep);
-    return o;
+// Warp-cooperative exact row group (all 32 lanes; lane j holds element j of tile row r, group g): the
+// reference's butterfly through shuffles (lower index the minuend), then
+//   status 1: the QuEST search of quest_search32 -- per-candidate errors summed by a warp tree (any fp32 order is
+//             within 31 u of the exact sum, far inside the 2^-14 near-tie guard), near-ties decided by the exact
+//             f64 search (quest_exact_cold) in lane 0;
+//   status 2: the exponent e is certain; codes and trust mask at e.
+// Every lane returns the group's codes, exponent and mask.
+static __device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+    for (int h = 16; h >= 1; h >>= 1) x = __fadd_rn(x, __shfl_xor_sync(0xffffffffu, x, h));
+    return x;
 }
-
-struct XqCol {
-    uint4 codes;
-    int e;
-};
-static __device__ __noinline__ XqCol xq_exact_col(const uint8_t* tile, int c, int g, uint32_t sw, float prescale,
-                                                  int* err) {
-    XqCol o;
-    exact_group(tile, true, c, g, sw, prescale, err, o.codes, o.e);
+static __device__ XqGroup xq_exact_row_warp(const uint8_t* tile, int r, int g, int status, int e_known, int* err) {
+    const int j = threadIdx.x & 31;
+    const uint16_t h16 = *reinterpret_cast<const uint16_t*>(tile + tq_off(r, 32 * g + j));
+    float v = __uint_as_float((uint32_t)h16 << 16);
+#pragma unroll
+    for (int h = 1; h < 32; h <<= 1) {
+        const float o = __shfl_xor_sync(0xffffffffu, v, h);
+        v = __fmul_rn((j & h) ? __fsub_rn(o, v) : __fadd_rn(v, o), kHc);
+    }
+    XqGroup o;
+    int e = e_known;
+    if (status == 1) {
+        float am = fabsf(v);
+#pragma unroll
+        for (int h = 1; h < 32; h <<= 1) am = max_nan2(am, __shfl_xor_sync(0xffffffffu, am, h));
+        if (!(am <= 3.4028234663852886e38f) && err && j == 0) atomicOr(err, 1);
+        if (!(am > 0.0f && am <= 3.4028234663852886e38f)) {   // zero group (or non-finite): _native.pyx:228-233
+            o.codes = make_uint4(0, 0, 0, 0);
+            o.keep = 0xFFFFFFFFu;
+            o.e = 0;
+            return o;
+        }
+        const int e_hi = ceil_scale_exp(am), e_lo = quest_low_exp(am);
+        e = e_hi;
+        if (e_hi > e_lo) {
+            const float sc0 = exp2i(127 - e_hi), a0 = __fmul_rn(am, sc0);
+            float best = __int_as_float(0x7f800000), second = best;
+            int bk = 0;
+            for (int k = 0; k <= e_hi - e_lo; ++k) {
+                const float sk = exp2i(k), ik = exp2i(-2 * k);
+                if (k >= 2) {
+                    const float d = __fsub_rn(__fmul_rn(a0, sk), 6.0f);
+                    const float lb = __fmul_rn(__fmul_rn(d, d), ik);
+                    if (__fmul_rn(lb, 0.99999905f) > __fadd_rn(__fmul_rn(best, 1.0f + kQTol), kQAtol)) break;
+                }
+                const float a = __fmul_rn(v, __fmul_rn(sc0, sk));
+                const uint32_t q = e2m1_rt_h2(a, 0.0f);
+                const float t = fh16_sub_lo(q, a);
+                const float ek = __fmul_rn(warp_sum(__fmul_rn(t, t)), ik);
+                if (ek < best) {
+                    second = best;
+                    best = ek;
+                    bk = k;
+                } else if (ek < second) {
+                    second = ek;
+                }
+            }
+            if (!(__fsub_rn(second, best) > __fadd_rn(__fmul_rn(second, kQTol), kQAtol))) {
+                float xs[32];   // near-tie: the exact sequential f64 search of the reference, in lane 0
+#pragma unroll
+                for (int i = 0; i < 32; ++i) xs[i] = __shfl_sync(0xffffffffu, v, i);
+                int ex = 0;
+                if (j == 0) ex = quest_exact_cold(xs, e_hi, e_lo);
+                e = __shfl_sync(0xffffffffu, ex, 0);
+            } else {
+                e = e_hi - bk;
+            }
+        }
+    }
+    const float a = __fmul_rn(v, exp2i(127 - e));
+    uint32_t nib = e2m1b(a, 0.0f) & 0xFu;
+    if ((nib & 7u) == 0) nib = 0;
+    const bool clip = (__float_as_uint(__fsub_rn(6.0f, fabsf(a))) >> 31) != 0;
+    o.keep = ~__ballot_sync(0xffffffffu, clip);
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[q] = __reduce_or_sync(0xffffffffu, (j >> 3) == q ? nib << (4 * (j & 7)) : 0u);
+    o.codes = make_uint4(w[0], w[1], w[2], w[3]);
+    o.e = e;
     return o;
 }
 
@@ -381,12 +420,17 @@ __global__ void __launch_bounds__(kXqThreads, 1) k_tcq_xq(const __grid_constant_
                 } else {
                     st = quest_checked(acc, codes, e, keep);
                 }
-                if (st && valid) {
-                    if (a.fallbacks) atomicAdd(a.fallbacks + (st == 2 ? 2 : 0), 1);
-                    const XqGroup o = xq_exact_row(tile, li, g, st, e, a.row_out.err);
-                    codes = o.codes;
-                    e = o.e;
-                    keep = o.keep;
+                // undecided groups: the whole warp recomputes them exactly, one at a time (no diverged lane)
+                for (uint32_t todo = __ballot_sync(0xffffffffu, st && valid); todo; todo &= todo - 1) {
+                    const int f = __ffs(todo) - 1;
+                    const int stf = __shfl_sync(0xffffffffu, st, f), ef = __shfl_sync(0xffffffffu, e, f);
+                    if (a.fallbacks && lane == 0) atomicAdd(a.fallbacks + (stf == 2 ? 2 : 0), 1);
+                    const XqGroup o = xq_exact_row_warp(tile, quad * 32 + f, g, stf, ef, a.row_out.err);
+                    if (lane == f) {
+                        codes = o.codes;
+                        e = o.e;
+                        keep = o.keep;
+                    }
                 }
                 if (!valid) {
                     codes = make_uint4(0, 0, 0, 0);
@@ -439,15 +483,23 @@ __global__ void __launch_bounds__(kXqThreads, 1) k_tcq_xq(const __grid_constant_
                 } else {
                     ok = rtn_checked(acc, a.col_prescale, codes, e);
                 }
-                if (orow < a.C && gk < a.R) {
-                    if (!ok) {
-                        if (a.fallbacks) atomicAdd(a.fallbacks + 1, 1);
-                        const XqCol o = xq_exact_col(smem + kXqOffDeq + d * kXqDeq, li, g,
-                                                     a.sign_r ? __ldg(a.sign_r + (gk >> 5)) : 0u, a.col_prescale,
-                                                     a.col_out.err);
-                        codes = o.codes;
-                        e = o.e;
+                {
+                    const uint32_t sw = a.sign_r && gk < a.R ? __ldg(a.sign_r + (gk >> 5)) : 0u;
+                    for (uint32_t todo = __ballot_sync(0xffffffffu, !ok && orow < a.C && gk < a.R); todo;
+                         todo &= todo - 1) {
+                        const int f = __ffs(todo) - 1;
+                        if (a.fallbacks && lane == 0) atomicAdd(a.fallbacks + 1, 1);
+                        uint4 cx;
+                        int ex;
+                        exact_group_warp(smem + kXqOffDeq + d * kXqDeq, true, quad * 32 + f, g, sw, a.col_prescale,
+                                         a.col_out.err, cx, ex);
+                        if (lane == f) {
+                            codes = cx;
+                            e = ex;
+                        }
                     }
+                }
+                if (orow < a.C && gk < a.R) {
                     *reinterpret_cast<uint4*>(a.col_out.codes + orow * a.col_out.ldc + (gk >> 5) * 16) = codes;
                     a.col_out.sf[sf_offset(orow, gk >> 5, a.col_out.katoms)] = (uint8_t)e;
                 }
