@@ -138,6 +138,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Single-thread producer / MMA roles: poll with a fixed sleep between tries (QT_ROLE_SLEEP_NS, build flag), so
+// a role that waits a whole tile phase does not take issue slots from the epilogue warps of its scheduler.
+#ifndef QT_ROLE_SLEEP_NS
+#define QT_ROLE_SLEEP_NS 128
+#endif
+__device__ __forceinline__ void mbar_wait_role(uint64_t* bar, uint32_t parity) {
+#if QT_ROLE_SLEEP_NS > 0
+    const uint32_t addr = smem_u32(bar);
+    for (;;) {
+        uint32_t done;
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done)
+                     : "r"(addr), "r"(parity)
+                     : "memory");
+        if (done) break;
+        __nanosleep(QT_ROLE_SLEEP_NS);
+    }
+#else
+    mbar_wait(bar, parity);
+#endif
+}
+
 template <int HINT_NS>
 __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity) {
 #if QT_WAIT_HINT

@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kTqThreads, 1)
             const int s = it % kTqStages;
             const uint32_t ph = (it / kTqStages) & 1;
             const int64_t r0 = (t % nRT) * 128, c0 = (t / nRT) * 128;
-            mbar_wait_hint<1000>(&empty[s], ph ^ 1);
+            mbar_wait_role(&empty[s], ph ^ 1);
             if (lane == 0) {
                 mbar_arrive_expect_tx(&full[s], kTqA);
                 uint8_t* As = smem + s * kTqStage;
@@ -144,8 +144,8 @@ __global__ void __launch_bounds__(kTqThreads, 1)
             int it = 0;
             for (int64_t t = blockIdx.x; t < NT; t += gridDim.x, ++it) {
                 const int s = it % kTqStages, b = it & 1;
-                mbar_wait_hint<1000>(&tmem_empty[b], ((it >> 1) & 1) ^ 1);
-                mbar_wait_hint<1000>(&full[s], (it / kTqStages) & 1);
+                mbar_wait_role(&tmem_empty[b], ((it >> 1) & 1) ^ 1);
+                mbar_wait_role(&full[s], (it / kTqStages) & 1);
                 tc_fence_after();
                 const uint32_t As = smem_u32(smem + s * kTqStage), Bs = As + kTqA;
                 const uint32_t d0 = tmem + b * 256;

@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kXqThreads, 1) k_tcq_xq(const __grid_constant_
                 const int64_t t = blockIdx.x + (int64_t)it * gridDim.x;
                 const int s = it % kXqStages;
                 const int64_t r0 = (t % nRT) * 128, c0 = (t / nRT) * 128;
-                mbar_wait_hint<1000>(&empty[s], ((it / kXqStages) & 1) ^ 1);
+                mbar_wait_role(&empty[s], ((it / kXqStages) & 1) ^ 1);
                 mbar_arrive_expect_tx(&full[s], kXqIn);
                 tma_load_2d(smem + s * kXqIn, &tmX, &full[s], (int)c0, (int)r0);
                 tma_load_2d(smem + s * kXqIn + 16384, &tmX, &full[s], (int)c0 + 64, (int)r0);
@@ -350,8 +350,8 @@ __global__ void __launch_bounds__(kXqThreads, 1) k_tcq_xq(const __grid_constant_
             for (int it = 0; it <= ntiles; ++it) {
                 if (it < ntiles) {
                     const int s = it % kXqStages, b = it & 1;
-                    mbar_wait_hint<1000>(&rfree[b], ((it >> 1) & 1) ^ 1);
-                    mbar_wait_hint<1000>(&full[s], (it / kXqStages) & 1);
+                    mbar_wait_role(&rfree[b], ((it >> 1) & 1) ^ 1);
+                    mbar_wait_role(&full[s], (it / kXqStages) & 1);
                     tc_fence_after();
                     const uint32_t As = smem_u32(smem + s * kXqIn);
 #pragma unroll
@@ -365,8 +365,8 @@ __global__ void __launch_bounds__(kXqThreads, 1) k_tcq_xq(const __grid_constant_
                 }
                 if (it >= 1) {
                     const int jt = it - 1, d = jt & 1;
-                    mbar_wait_hint<1000>(&cfree[d], ((jt >> 1) & 1) ^ 1);
-                    mbar_wait_hint<1000>(&dfull[d], (jt >> 1) & 1);
+                    mbar_wait_role(&cfree[d], ((jt >> 1) & 1) ^ 1);
+                    mbar_wait_role(&dfull[d], (jt >> 1) & 1);
                     tc_fence_after();
                     const uint32_t Ds = smem_u32(smem + kXqOffDeq + d * kXqDeq), Bs = Ds + kXqDeqA;
 #pragma unroll
