@@ -409,21 +409,25 @@ def run_ours(args, rank, world, local_rank):
         ms = float(t.item())
     # the same step with stochastic-rounding backward operands (qlinear.py:168-175, rounding="sr"): the SR
     # quantizers run on the CUDA cores (the tensor-core dual quantizer is RTN-only)
-    sr = None
+    sr = {}
     if world == 1 and not args.no_graph:
-        g_sr, _ = capture(lambda: step(args.warmup + 2, rounding="sr"))
-        g_sr.replay()
-        torch.cuda.synchronize()
-        s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record()
-        for _ in range(args.steps):
+        for mode, what in (("sr", "same step, backward rounding 'sr' (G, G_t, W_t, X_t by SR on the reference's "
+                                  "splitmix64 stream, bit-exact)"),
+                           ("sr_fast", "same step, backward rounding 'sr_fast' (B200 extension: the same SR "
+                                       "decisions against 24-bit hash uniforms; statistically unbiased)")):
+            g_sr, _ = capture(lambda m=mode: step(args.warmup + 2, rounding=m))
             g_sr.replay()
-        e0.record()
-        torch.cuda.synchronize()
-        sr_ms = s0.elapsed_time(e0) / args.steps
-        sr = {"value": round(flops_per_step(T) / (sr_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
-              "ms_per_step": round(sr_ms, 4), "what": "same step, backward rounding 'sr' (G, G_t, W_t, X_t by SR)"}
-        del g_sr
+            torch.cuda.synchronize()
+            s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            for _ in range(args.steps):
+                g_sr.replay()
+            e0.record()
+            torch.cuda.synchronize()
+            sr_ms = s0.elapsed_time(e0) / args.steps
+            sr[mode] = {"value": round(flops_per_step(T) / (sr_ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+                        "ms_per_step": round(sr_ms, 4), "what": what}
+            del g_sr
     # end to end at N GPUs: every rank streams its own shard through its own PCIe link; max over ranks
     if world > 1:
         dist.barrier()
@@ -499,7 +503,8 @@ def run_ours(args, rank, world, local_rank):
                                "unit": "GB/s", "frac": round(q_gbs / peaks["hbm_gbs"], 4),
                                "share_of_step": round(q_us * 1e-3 / ms, 4)},
         "kernels": table,
-        "sr_backward": sr,
+        "sr_backward": sr.get("sr"),
+        "sr_fast_backward": sr.get("sr_fast"),
         "e2e": e2e,
         # per step and shape: 2 sign bitmaps + 2 fused forward quantizers + 1 GEMM; 1 dual quantizer + 2 GEMMs
         "gpu_launches": 7 * len(SHAPES) * args.steps,  # signs pair, fused X, fused W, GEMM, dual dy, 2 GEMMs
@@ -520,7 +525,7 @@ def run_train(rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     out = {"data": "synthetic token streams (no datasets offline)",
            "optimizer": "AdamW 0.9/0.95 wd 0.1, clip 1.0, warmup+cosine (train.py:58-85, 325-382)"}
-    for key, args in (("llama200m_dp", ("200m", 64, 5, 2, False)), ("llama30m", ("30m", 64, 3, 1, False)),
+    for key, args in (("llama200m_dp", ("200m", 64, 5, 3, False)), ("llama30m", ("30m", 64, 5, 3, False)),
                       ("block7b_8k_b4", ("7b", 4, 3, 1, True))):
         q = run(llama, *args, dev, world, rank, "quartet")
         torch.cuda.empty_cache()

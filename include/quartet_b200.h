@@ -68,6 +68,10 @@ extern "C" {
 #define QT_ROUND_QUEST 0           /* quantize_quest, ratio_lo = 1/16 (_native.pyx:206-245) */
 #define QT_ROUND_RTN 1             /* quantize_rtn (_native.pyx:104-131) */
 #define QT_ROUND_SR 2              /* quantize_sr (_native.pyx:134-168) */
+#define QT_ROUND_SR_FAST 3         /* B200 extension: stochastic rounding with the same neighbours and p as QT_ROUND_SR,
+                                      against 24-bit uniforms from a 32-bit hash of (seed, stream position) --
+                                      statistically unbiased, not the reference's splitmix64 draws (quantizer entry
+                                      points only; the seam and the diagnostics keep the reference's streams) */
 #define QT_EPI_STORE 0             /* D = A B^T */
 #define QT_EPI_MASK_H 1            /* D = H32(A B^T (.) mask) * scale (qlinear.py:229-230, 249-250) */
 #define QT_EPI_MASK 2              /* D = (A B^T (.) mask) * scale (hadamard=False layers) */
@@ -98,6 +102,15 @@ QT_API int qt_sign_bits_at(uint32_t* d_bits, int64_t start, int64_t n, uint64_t 
  * into b (a layer's d_out and token signs; same bitmaps as two qt_sign_bits_at calls). */
 QT_API int qt_sign_bits_pair(uint32_t* a, int64_t start_a, int64_t n_a, uint32_t* b, int64_t start_b, int64_t n_b,
                              uint64_t xi, void* stream);
+
+/* Device-resident seeds, for a training step captured as one CUDA graph (the seed changes every step):
+ * qt_layer_seeds writes d_xi[l] = derive_seed(derive_seed(seed, 4, *d_step), d_layer_ids[l]) for l < n -- the
+ * per-step, per-layer backward seed of the reference's training loop (train.py:346-348) -- and then increments
+ * *d_step if `increment`; qt_sign_bits_pair_dev is qt_sign_bits_pair with xi = *d_xi read on the device. */
+QT_API int qt_layer_seeds(uint64_t* d_xi, const uint64_t* d_layer_ids, int n, uint64_t seed, int64_t* d_step,
+                          int increment, void* stream);
+QT_API int qt_sign_bits_pair_dev(uint32_t* a, int64_t start_a, int64_t n_a, uint32_t* b, int64_t start_b, int64_t n_b,
+                                 const uint64_t* d_xi, void* stream);
 
 /* Blockwise transform only (the kernels.fwht plugin entry, _native.pyx:353-379, with the
  * randomized variant of hadamard.py:82-85): out[r, :] = prescale * FWHT32(x[r, :] (.) s), fp32,

@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("QT_LIB_PATH") or os.path.join(HERE, "_build", "libqua
 
 QT_IN_BF16, QT_IN_F32, QT_IN_MXFP4 = 0, 1, 2
 QT_TRANSFORM_NONE, QT_TRANSFORM_HADAMARD, QT_TRANSFORM_RANDOMIZED = 0, 1, 2
-QT_ROUND_QUEST, QT_ROUND_RTN, QT_ROUND_SR = 0, 1, 2
+QT_ROUND_QUEST, QT_ROUND_RTN, QT_ROUND_SR, QT_ROUND_SR_FAST = 0, 1, 2, 3
 QT_EPI_STORE, QT_EPI_MASK_H, QT_EPI_MASK = 0, 1, 2
 QT_EPI_ACCUMULATE = 0x10
 QT_OUT_F32, QT_OUT_BF16 = 0, 1
@@ -33,6 +33,8 @@ SIGNATURES = {
     "qt_sign_bits": (_i32, [_vp, _i64, _u64, _vp]),
     "qt_sign_bits_at": (_i32, [_vp, _i64, _i64, _u64, _vp]),
     "qt_sign_bits_pair": (_i32, [_vp, _i64, _i64, _vp, _i64, _i64, _u64, _vp]),
+    "qt_sign_bits_pair_dev": (_i32, [_vp, _i64, _i64, _vp, _i64, _i64, _vp, _vp]),
+    "qt_layer_seeds": (_i32, [_vp, _vp, _i32, _u64, _vp, _i32, _vp]),
     "qt_debug_set_gemm": (None, [_i32]),
     "qt_debug_set_grid": (None, [_i32]),
     "qt_debug_set_quant": (None, [_i32, _vp]),

@@ -8,6 +8,8 @@ using namespace qt;
 
 static inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 static inline uint64_t sr_base_of(uint64_t seed) { return mix64(seed ^ mix64(kDomainSR)); }
+// QT_ROUND_SR_FAST runs the SR kernels with the hash uniforms (QuantCfg::sr_fast)
+static inline int round_kind(int r) { return r == QT_ROUND_SR_FAST ? QT_ROUND_SR : r; }
 
 static int g_gemm_dbg = 0;  // experiment knobs for qt_debug_set_gemm (never set in production)
 static int g_quant_mode = 0;  // qt_debug_set_quant: 0 production (tensor-core quantizers where they apply), 1 CUDA cores only
@@ -98,6 +100,18 @@ int qt_sign_bits_pair(uint32_t* a, int64_t start_a, int64_t n_a, uint32_t* b, in
     return launch_signs2(a, start_a, n_a, b, start_b, n_b, xi, (cudaStream_t)stream);
 }
 
+int qt_sign_bits_pair_dev(uint32_t* a, int64_t start_a, int64_t n_a, uint32_t* b, int64_t start_b, int64_t n_b,
+                          const uint64_t* d_xi, void* stream) {
+    if (start_a < 0 || start_b < 0 || n_a < 0 || n_b < 0 || !d_xi) return QT_ERR_ARG;
+    return launch_signs2_dev(a, start_a, n_a, b, start_b, n_b, d_xi, (cudaStream_t)stream);
+}
+
+int qt_layer_seeds(uint64_t* d_xi, const uint64_t* d_layer_ids, int n, uint64_t seed, int64_t* d_step, int increment,
+                   void* stream) {
+    if (n < 0 || (n > 0 && (!d_xi || !d_layer_ids)) || !d_step) return QT_ERR_ARG;
+    return launch_layer_seeds(d_xi, d_layer_ids, n, seed, d_step, increment, (cudaStream_t)stream);
+}
+
 // ---- exact plugin seam (seam.cu): f64 / any-group replays of _native.pyx:104-396
 int qt_seam_quantize(const double* x, int64_t rows, int64_t cols, int64_t group, int rounding, int values,
                      uint64_t seed, uint64_t counter_start, double ratio_lo, uint8_t* codes, uint8_t* scales,
@@ -143,12 +157,13 @@ int qt_quant_rows(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_
                   void* stream) {
     if (cols % 32 != 0 || rows < 0) return QT_ERR_SHAPE;
     if (in_dtype != QT_IN_BF16 && in_dtype != QT_IN_F32) return QT_ERR_ARG;
-    if (rounding < 0 || rounding > 2 || transform < 0 || transform > 2) return QT_ERR_ARG;
+    if (rounding < 0 || rounding > 3 || transform < 0 || transform > 2) return QT_ERR_ARG;
     if (rows == 0 || cols == 0) return 0;  // nothing to quantize: no pointer is read (empty sign vectors are null)
     if (transform == QT_TRANSFORM_RANDOMIZED && !sign_bits) return QT_ERR_ARG;
     int esz = in_dtype == QT_IN_BF16 ? 2 : 4;
     if (!al16(x) || (ldx * esz) % 16 || !al16(codes) || ldc % 16) return QT_ERR_ALIGN;
-    QuantCfg cfg{transform, sign_bits, prescale, rounding, sr_base_of(sr_seed), counter_start, counter_ld};
+    QuantCfg cfg{transform, sign_bits, prescale, round_kind(rounding), sr_base_of(sr_seed), counter_start, counter_ld,
+                 rounding == QT_ROUND_SR_FAST};
     QuantOut out{codes, ldc, sf, katoms, mask, err, fallbacks};
     return launch_quant_rows(x, in_dtype, ldx, rows, cols, cfg, out, (cudaStream_t)stream);
 }
@@ -159,7 +174,7 @@ int qt_quant_cols(const void* x, int in_dtype, int64_t ldx, const uint8_t* mx_co
                   int64_t counter_ld, uint8_t* codes, int64_t ldc, uint8_t* sf, int64_t katoms, int* err,
                   void* stream) {
     if (rows % 32 != 0 || cols % 32 != 0 || rows < 0 || cols < 0) return QT_ERR_SHAPE;
-    if (in_dtype < 0 || in_dtype > 2 || rounding < 0 || rounding > 2 || transform < 0 || transform > 2)
+    if (in_dtype < 0 || in_dtype > 2 || rounding < 0 || rounding > 3 || transform < 0 || transform > 2)
         return QT_ERR_ARG;
     if (rows == 0 || cols == 0) return 0;  // nothing to quantize: no pointer is read (empty sign vectors are null)
     if (transform == QT_TRANSFORM_RANDOMIZED && !sign_bits) return QT_ERR_ARG;
@@ -170,7 +185,8 @@ int qt_quant_cols(const void* x, int in_dtype, int64_t ldx, const uint8_t* mx_co
         if (!al16(x) || (ldx * esz) % 16) return QT_ERR_ALIGN;
     }
     if (!al16(codes) || ldc % 16) return QT_ERR_ALIGN;
-    QuantCfg cfg{transform, sign_bits, prescale, rounding, sr_base_of(sr_seed), counter_start, counter_ld};
+    QuantCfg cfg{transform, sign_bits, prescale, round_kind(rounding), sr_base_of(sr_seed), counter_start, counter_ld,
+                 rounding == QT_ROUND_SR_FAST};
     QuantOut out{codes, ldc, sf, katoms, nullptr, err, nullptr};
     MxIn mx{mx_codes, mx_ldc, mx_sf, mx_katoms};
     return launch_quant_tile(x, in_dtype, ldx, mx, rows, cols, nullptr, nullptr, &cfg, &out, 0, (cudaStream_t)stream);
@@ -183,7 +199,7 @@ int qt_quant_dual(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_
                   uint32_t* row_mask, uint8_t* col_codes, int64_t col_ldc, uint8_t* col_sf, int64_t col_katoms,
                   int* err, void* stream) {
     if (rows % 32 != 0 || cols % 32 != 0 || rows < 0 || cols < 0) return QT_ERR_SHAPE;
-    if ((in_dtype != QT_IN_BF16 && in_dtype != QT_IN_F32) || rounding < 0 || rounding > 2 || transform < 0 ||
+    if ((in_dtype != QT_IN_BF16 && in_dtype != QT_IN_F32) || rounding < 0 || rounding > 3 || transform < 0 ||
         transform > 2)
         return QT_ERR_ARG;
     if (rows == 0 || cols == 0) return 0;  // nothing to quantize: no pointer is read (empty sign vectors are null)
@@ -191,9 +207,10 @@ int qt_quant_dual(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_
     int esz = in_dtype == QT_IN_BF16 ? 2 : 4;
     if (!al16(x) || (ldx * esz) % 16 || !al16(row_codes) || row_ldc % 16 || !al16(col_codes) || col_ldc % 16)
         return QT_ERR_ALIGN;
-    QuantCfg rc{transform, row_sign_bits, prescale, rounding, sr_base_of(seed_rows), row_counter_start, 0};
-    QuantCfg cc{transform, col_sign_bits, prescale, rounding, sr_base_of(seed_cols), col_counter_start,
-                col_counter_ld};
+    QuantCfg rc{transform, row_sign_bits, prescale, round_kind(rounding), sr_base_of(seed_rows), row_counter_start, 0,
+                rounding == QT_ROUND_SR_FAST};
+    QuantCfg cc{transform, col_sign_bits, prescale, round_kind(rounding), sr_base_of(seed_cols), col_counter_start,
+                col_counter_ld, rounding == QT_ROUND_SR_FAST};
     QuantOut ro{row_codes, row_ldc, row_sf, row_katoms, row_mask, err, nullptr};
     QuantOut co{col_codes, col_ldc, col_sf, col_katoms, nullptr, err, nullptr};
     if (g_quant_mode == 0 && in_dtype == QT_IN_BF16 && rounding == QT_ROUND_RTN &&
@@ -216,7 +233,7 @@ int qt_quant_fused(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64
                    uint8_t* col_sf, int64_t col_katoms, int* err, int* fallbacks, void* stream) {
     if (rows % 32 != 0 || cols % 32 != 0 || rows < 0 || cols < 0) return QT_ERR_SHAPE;
     if (in_dtype != QT_IN_BF16 && in_dtype != QT_IN_F32) return QT_ERR_ARG;
-    if (row_rounding < 0 || row_rounding > 2 || col_rounding < 1 || col_rounding > 2) return QT_ERR_ARG;
+    if (row_rounding < 0 || row_rounding > 3 || col_rounding < 1 || col_rounding > 3) return QT_ERR_ARG;
     if (row_transform < 0 || row_transform > 2 || col_transform < 0 || col_transform > 2) return QT_ERR_ARG;
     if (rows == 0 || cols == 0) return 0;  // nothing to quantize: no pointer is read (empty sign vectors are null)
     if ((row_transform == QT_TRANSFORM_RANDOMIZED && !row_sign_bits) ||
@@ -225,10 +242,10 @@ int qt_quant_fused(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64
     int esz = in_dtype == QT_IN_BF16 ? 2 : 4;
     if (!al16(x) || (ldx * esz) % 16 || !al16(row_codes) || row_ldc % 16 || !al16(col_codes) || col_ldc % 16)
         return QT_ERR_ALIGN;
-    QuantCfg rc{row_transform, row_sign_bits, row_prescale, row_rounding, sr_base_of(row_seed), row_counter_start,
-                row_counter_ld};
-    QuantCfg cc{col_transform, col_sign_bits, col_prescale, col_rounding, sr_base_of(col_seed), col_counter_start,
-                col_counter_ld};
+    QuantCfg rc{row_transform, row_sign_bits, row_prescale, round_kind(row_rounding), sr_base_of(row_seed),
+                row_counter_start, row_counter_ld, row_rounding == QT_ROUND_SR_FAST};
+    QuantCfg cc{col_transform, col_sign_bits, col_prescale, round_kind(col_rounding), sr_base_of(col_seed),
+                col_counter_start, col_counter_ld, col_rounding == QT_ROUND_SR_FAST};
     QuantOut ro{row_codes, row_ldc, row_sf, row_katoms, row_mask, err, fallbacks};
     QuantOut co{col_codes, col_ldc, col_sf, col_katoms, nullptr, err, nullptr};
     if (g_quant_mode != 1 && in_dtype == QT_IN_BF16 && row_rounding == QT_ROUND_QUEST &&

@@ -27,6 +27,7 @@ struct QuantCfg {
     uint64_t sr_base;           // mix64(seed ^ mix64(DOMAIN_SR))
     uint64_t counter_start;
     int64_t counter_ld;         // SR stream row stride (0 = the quantized matrix's own row length)
+    int sr_fast;                // rounding kSr only: 1 = QT_ROUND_SR_FAST (hash uniforms, not the reference stream)
 };
 
 struct MxIn {
@@ -64,6 +65,10 @@ int launch_transform_rows(const float* x, float* out, int64_t rows, int64_t cols
 int launch_signs(uint32_t* bits, int64_t start, int64_t n, uint64_t xi, cudaStream_t st);
 int launch_signs2(uint32_t* a, int64_t sa, int64_t na, uint32_t* b, int64_t sb, int64_t nb, uint64_t xi,
                   cudaStream_t st);
+int launch_signs2_dev(uint32_t* a, int64_t sa, int64_t na, uint32_t* b, int64_t sb, int64_t nb, const uint64_t* xi,
+                      cudaStream_t st);
+int launch_layer_seeds(uint64_t* xi, const uint64_t* ids, int n, uint64_t seed, int64_t* step, int inc,
+                       cudaStream_t st);
 int launch_quant_rows(const void* x, int in_type, int64_t ldx, int64_t rows, int64_t cols, const QuantCfg& cfg,
                       const QuantOut& out, cudaStream_t st);
 int launch_quant_tile(const void* x, int in_type, int64_t ldx, const MxIn& mx, int64_t R, int64_t C,

@@ -287,15 +287,29 @@ __device__ __forceinline__ int quant_group(float (&v)[32], const QuantCfg& cf, u
         const float sc_f = exp2i(127 - e);
         const double sc_d = (double)sc_f;
         uint32_t w[4];
+        if (cf.sr_fast) {   // QT_ROUND_SR_FAST: statistically unbiased, not the reference's stream
+            const uint32_t k0 = (uint32_t)cf.sr_base, k1 = (uint32_t)(cf.sr_base >> 32);
 #pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-            uint32_t acc = 0;
+            for (int qq = 0; qq < 4; ++qq) {
+                uint32_t acc = 0;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int j = qq * 8 + k;
-                acc |= sr_code(v[j], sc_f, sc_d, cf.sr_base, sr_idx + (uint64_t)j) << (4 * k);
+                for (int k = 0; k < 8; ++k) {
+                    const int j = qq * 8 + k;
+                    acc |= sr_code_fast(v[j], sc_f, k0, k1, sr_idx + (uint64_t)j) << (4 * k);
+                }
+                w[qq] = acc;
             }
-            w[qq] = acc;
+        } else {
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int j = qq * 8 + k;
+                    acc |= sr_code(v[j], sc_f, sc_d, cf.sr_base, sr_idx + (uint64_t)j) << (4 * k);
+                }
+                w[qq] = acc;
+            }
         }
         codes = make_uint4(w[0], w[1], w[2], w[3]);
     }

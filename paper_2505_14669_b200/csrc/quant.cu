@@ -46,6 +46,31 @@ __global__ void k_signs2(uint32_t* a, int64_t sa, int64_t na, int64_t nba, uint3
         signs_word(b, sb, nb, base, w);
     }
 }
+// k_signs2 with the seed read from device memory: the per-step layer seeds of a captured training step
+__global__ void k_signs2_dev(uint32_t* a, int64_t sa, int64_t na, int64_t nba, uint32_t* b, int64_t sb, int64_t nb,
+                             const uint64_t* xi) {
+    const uint64_t base = mix64(*xi ^ mix64(kDomainSigns));
+    const bool first = blockIdx.x < nba;
+    const int64_t w = (first ? blockIdx.x : blockIdx.x - nba) * (int64_t)blockDim.x + threadIdx.x;
+    if (first) {
+        if (w < (na + 31) / 32) signs_word(a, sa, na, base, w);
+    } else if (w < (nb + 31) / 32) {
+        signs_word(b, sb, nb, base, w);
+    }
+}
+
+__device__ __forceinline__ uint64_t derive2(uint64_t acc, uint64_t p) {  // one fold of rng.derive_seed
+    return mix64(acc ^ p) + kGolden;
+}
+// xi[l] = derive_seed(derive_seed(seed, 4, *step), ids[l]) (train.py:346-348), then ++*step: one block
+__global__ void k_layer_seeds(uint64_t* xi, const uint64_t* ids, int n, uint64_t seed, int64_t* step, int inc) {
+    const uint64_t s = (uint64_t)*step;
+    const uint64_t d = mix64(derive2(derive2(derive2(0x243F6A8885A308D3ULL, seed), 4), s));
+    for (int l = threadIdx.x; l < n; l += blockDim.x) xi[l] = mix64(derive2(derive2(0x243F6A8885A308D3ULL, d), ids[l]));
+    __syncthreads();
+    if (threadIdx.x == 0 && inc) *step = (int64_t)(s + 1);
+}
+
 __global__ void k_signs(uint32_t* bits, int64_t start, int64_t n, uint64_t base) {
     int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t nw = (n + 31) / 32;
@@ -492,6 +517,20 @@ int launch_signs2(uint32_t* a, int64_t sa, int64_t na, uint32_t* b, int64_t sb, 
     const int64_t nba = ((na + 31) / 32 + 255) / 256, nbb = ((nb + 31) / 32 + 255) / 256;
     if (nba + nbb == 0) return 0;
     k_signs2<<<(unsigned)(nba + nbb), 256, 0, st>>>(a, sa, na, nba, b, sb, nb, base);
+    return (int)cudaGetLastError();
+}
+
+int launch_signs2_dev(uint32_t* a, int64_t sa, int64_t na, uint32_t* b, int64_t sb, int64_t nb, const uint64_t* xi,
+                      cudaStream_t st) {
+    const int64_t nba = ((na + 31) / 32 + 255) / 256, nbb = ((nb + 31) / 32 + 255) / 256;
+    if (nba + nbb == 0) return 0;
+    k_signs2_dev<<<(unsigned)(nba + nbb), 256, 0, st>>>(a, sa, na, nba, b, sb, nb, xi);
+    return (int)cudaGetLastError();
+}
+
+int launch_layer_seeds(uint64_t* xi, const uint64_t* ids, int n, uint64_t seed, int64_t* step, int inc,
+                       cudaStream_t st) {
+    k_layer_seeds<<<1, 256, 0, st>>>(xi, ids, n, seed, step, inc);
     return (int)cudaGetLastError();
 }
 

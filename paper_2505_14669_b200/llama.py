@@ -26,7 +26,7 @@ import torch.nn.functional as F
 
 from . import _lib
 from .mxfp4 import _stream
-from .nn import QuartetLinear, quartet_linear_group, set_token_shard
+from .nn import QuartetLinear, nonfinite_flag, quartet_linear_group, set_token_shard
 
 GROUP = 32
 
@@ -270,6 +270,7 @@ class LlamaQuartet(torch.nn.Module):
     def __init__(self, cfg: LlamaConfig, seed: int = 0, device=None, blocks_only: bool = False):
         super().__init__()
         self.cfg = cfg
+        self._seeds = None
         g = torch.Generator(device="cpu").manual_seed(seed)
         self.embed = None if blocks_only else torch.nn.Parameter(
             (torch.randn(cfg.vocab, cfg.d_model, generator=g) * 0.02).to(device))
@@ -287,7 +288,36 @@ class LlamaQuartet(torch.nn.Module):
         self.register_buffer("cos", cos, persistent=False)
         self.register_buffer("sin", sin, persistent=False)
 
+    def use_device_seeds(self) -> None:
+        """Keep the per-step, per-layer backward seeds on the device (for a training step captured as one CUDA
+        graph): every forward in training mode first runs qt_layer_seeds -- xi_l = derive_seed(derive_seed(seed,
+        4, step), layer_l) for all Quartet layers, step++ (train.py:346-348, the same values QuartetLinear.xi()
+        computes on the host) -- and the layers' sign kernels read xi_l from there.  RTN backward only."""
+        mods = [m for m in self.modules() if isinstance(m, QuartetLinear)]
+        if not mods or self._seeds is not None:
+            return
+        steps = {m.step for m in mods}
+        seeds = {m.seed for m in mods}
+        if len(steps) != 1 or len(seeds) != 1 or any(m.rounding != "rtn" for m in mods):
+            raise ValueError("device seeds need Quartet layers at the same step with one seed and rtn rounding")
+        dev = mods[0].weight.device
+        ids = torch.tensor([m.layer_id for m in mods], dtype=torch.int64, device=dev)
+        xi = torch.zeros(len(mods), dtype=torch.int64, device=dev)
+        step = torch.tensor([steps.pop()], dtype=torch.int64, device=dev)
+        for i, m in enumerate(mods):
+            m.xi_slot = (xi, i)
+        self._seeds = (xi, ids, step, seeds.pop(), len(mods))
+
+    def _launch_seeds(self) -> None:
+        xi, ids, step, seed, n = self._seeds
+        rc = _lib.load().qt_layer_seeds(xi.data_ptr(), ids.data_ptr(), n, seed & 0xFFFFFFFFFFFFFFFF, step.data_ptr(),
+                                        1, _stream(xi.device))
+        if rc:
+            raise RuntimeError(f"qt_layer_seeds failed: {rc}")
+
     def forward(self, tokens=None, x=None):
+        if self._seeds is not None and self.training:
+            self._launch_seeds()
         if x is None:
             x = F.embedding(tokens, self.embed).to(torch.bfloat16)
         for blk in self.blocks:
@@ -411,13 +441,32 @@ class Trainer:
     """AdamW / clip / schedule of the reference loop (train.py:325-382) around LlamaQuartet, data parallel."""
 
     def __init__(self, model: torch.nn.Module, steps: int, lr: float, weight_decay: float = 0.1,
-                 grad_clip: float = 1.0, betas=(0.9, 0.95), eps: float = 1e-8):
+                 grad_clip: float = 1.0, betas=(0.9, 0.95), eps: float = 1e-8, graph: bool = False):
+        """graph=True (one GPU): after two eager warm-up steps the whole training step -- forward, loss,
+        backward, clipping, AdamW -- is captured once as a CUDA graph and replayed, with the per-step layer
+        seeds (LlamaQuartet.use_device_seeds) and the learning rate (a device scalar) updated on the device, so
+        the host launches one graph per step instead of ~1000 kernels."""
         self.model, self.steps, self.lr, self.grad_clip = model, steps, lr, grad_clip
         params = [p for p in model.parameters() if p.requires_grad]
-        self.opt = torch.optim.AdamW(params, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay,
-                                     fused=params[0].is_cuda)
+        self.graph = bool(graph)
+        if self.graph:
+            self.lr_t = torch.tensor(float(lr_at(0, steps, lr)), dtype=torch.float32, device=params[0].device)
+            self.opt = torch.optim.AdamW(params, lr=self.lr_t, betas=betas, eps=eps, weight_decay=weight_decay,
+                                         fused=True, capturable=True)
+            if hasattr(model, "use_device_seeds"):
+                model.use_device_seeds()
+        else:
+            self.opt = torch.optim.AdamW(params, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay,
+                                         fused=params[0].is_cuda)
+        self._cuda_graph = None
         self.bucket = OverlappedGradBuckets(params)
         self.step_i = 0
+        # non-finite quantizer inputs (the reference raises / stops on them, codec.py:164-170,
+        # train.py:341-343): the Quartet layers OR them into a device flag; each step copies it to pinned host
+        # memory without a sync and the NEXT step checks the copy, so the check never stalls the launch queue
+        dev = params[0].device
+        self._flag = nonfinite_flag(dev) if dev.type == "cuda" else None
+        self._pending: list = []   # (step, pinned host copy of the flag, event) not yet known to be complete
         import torch.distributed as dist
 
         if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
@@ -440,7 +489,65 @@ class Trainer:
             set_token_shard(self.model, 0, None)
         self._shard_tokens = n_tokens
 
+    def check_finite(self, wait: bool = False) -> None:
+        """Raise ValueError if a finished step quantized a non-finite value.  Without `wait` only the copies
+        whose events have completed are read (event.query(), never a stall of the launch queue), so a
+        divergence is reported a step or two after it happened; wait=True checks every step so far."""
+        while self._pending:
+            step, host, ev = self._pending[0]
+            if not wait and not ev.query():
+                break
+            ev.synchronize()
+            self._pending.pop(0)
+            if int(host.item()) != 0:
+                self._flag.zero_()
+                self._pending.clear()
+                raise ValueError(f"non-finite input to a Quartet layer at or before step {step} (training diverged)")
+
+    def _body(self, tokens, targets):
+        logits = self.model(tokens)
+        loss = cross_entropy(logits.view(-1, logits.shape[-1]), targets.reshape(-1))
+        loss.backward()
+        self.bucket.finish()
+        torch.nn.utils.clip_grad_norm_(self.bucket.params, self.grad_clip, foreach=True)
+        self.opt.step()
+        return loss.detach()
+
+    def _graph_step(self, tokens, targets) -> torch.Tensor:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            raise NotImplementedError("graph=True captures a one-GPU step (the bucket all-reduces run eagerly)")
+        self.lr_t.fill_(lr_at(self.step_i, self.steps, self.lr))
+        if self._cuda_graph is None and self.step_i >= 2:
+            self._tok, self._tgt = tokens.clone(), targets.clone()
+            self.opt.zero_grad(set_to_none=True)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._loss = self._body(self._tok, self._tgt)
+            self._cuda_graph = g
+            # the capture only recorded the step: run it (the capture advanced no state on the device)
+        if self._cuda_graph is None:   # warm-up steps (optimizer state, kernels' one-time setup) on a side stream
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                self.opt.zero_grad(set_to_none=True)
+                loss = self._body(tokens, targets)
+            torch.cuda.current_stream().wait_stream(st)
+            return loss
+        if tokens.data_ptr() != self._tok.data_ptr():
+            self._tok.copy_(tokens, non_blocking=True)
+            self._tgt.copy_(targets, non_blocking=True)
+        self._cuda_graph.replay()
+        return self._loss
+
     def step(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        self.check_finite()
+        if self.graph:
+            self._place_shard(tokens.numel())
+            loss = self._graph_step(tokens, targets)
+            self._after_step()
+            return loss
         self._place_shard(tokens.numel())
         lr = lr_at(self.step_i, self.steps, self.lr)
         for gr in self.opt.param_groups:
@@ -452,8 +559,17 @@ class Trainer:
         self.bucket.finish()
         torch.nn.utils.clip_grad_norm_(self.bucket.params, self.grad_clip)
         self.opt.step()
-        self.step_i += 1
+        self._after_step()
         return loss.detach()
+
+    def _after_step(self) -> None:
+        if self._flag is not None:
+            host = torch.empty(1, dtype=torch.int32, pin_memory=True)
+            host.copy_(self._flag, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._pending.append((self.step_i, host, ev))
+        self.step_i += 1
 
 
 def synthetic_batch(cfg: LlamaConfig, batch: int, seed: int, device) -> tuple[torch.Tensor, torch.Tensor]:

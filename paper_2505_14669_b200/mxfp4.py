@@ -119,6 +119,17 @@ def sign_bits_pair(xi: int, n_a: int, n_b: int, device, start_a: int = 0, start_
     return a, b
 
 
+def sign_bits_pair_dev(xi_slot, n_a: int, n_b: int, device, start_a: int = 0, start_b: int = 0):
+    """sign_bits_pair with xi read on the device: xi_slot = (uint64 tensor, index) -- the seed of the current
+    training step inside a captured CUDA graph (qt_sign_bits_pair_dev)."""
+    buf, idx = xi_slot
+    a = torch.empty(((n_a + 31) // 32,), dtype=torch.int32, device=device)
+    b = torch.empty(((n_b + 31) // 32,), dtype=torch.int32, device=device)
+    check(_lib.load().qt_sign_bits_pair_dev(a.data_ptr(), int(start_a), n_a, b.data_ptr(), int(start_b), n_b,
+                                            buf.data_ptr() + 8 * int(idx), _stream(a.device)), "qt_sign_bits_pair_dev")
+    return a, b
+
+
 def fwht32(x: torch.Tensor, transform: int = 1, signs: torch.Tensor | None = None,
            prescale: float = 1.0) -> torch.Tensor:
     """prescale * FWHT32(x (.) s) along the last axis, fp32 (kernels.fwht, _native.pyx:353-379)."""

@@ -20,10 +20,38 @@ from . import qlinear
 from .mxfp4 import derive_seed
 
 
+DEVICE_XI = -1   # placeholder xi of layers whose seed is device-resident (matches forward's eager operands)
+_NONFINITE: dict = {}
+
+
+def nonfinite_flag(device) -> torch.Tensor:
+    """The per-device flag the autograd path ORs non-finite quantizer inputs into (no host sync per call; the
+    reference raises ValueError("non-finite input") at once, codec.py:164-170)."""
+    dev = torch.device(device)
+    if dev not in _NONFINITE:
+        _NONFINITE[dev] = torch.zeros(1, dtype=torch.int32, device=dev)
+    return _NONFINITE[dev]
+
+
+def raise_if_nonfinite(device=None) -> None:
+    """One host sync: raise ValueError if any Quartet layer on `device` (default: all) quantized a non-finite
+    value since the last call, and clear the flag.  The training loop calls it once per step, after backward
+    (the reference's loop stops on a non-finite loss, train.py:341-343)."""
+    devs = [torch.device(device)] if device is not None else list(_NONFINITE)
+    bad = False
+    for d in devs:
+        f = _NONFINITE.get(d)
+        if f is not None and int(f.item()) != 0:
+            f.zero_()
+            bad = True
+    if bad:
+        raise ValueError("non-finite input")
+
+
 class QuartetLinearFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, w, xi: int, rounding: str = "rtn", hadamard: bool = True,
-                scheme: qlinear.QuantScheme = qlinear.QUEST, shard: tuple = (0, None)):
+                scheme: qlinear.QuantScheme = qlinear.QUEST, shard: tuple = (0, None), xi_dev=None):
         lead = x.shape[:-1]
         x2 = x.reshape(-1, x.shape[-1])
         if x2.dtype not in (torch.bfloat16, torch.float32):
@@ -32,8 +60,8 @@ class QuartetLinearFn(torch.autograd.Function):
         # xi is known now, so X_t / W_t come out of the same read of x / w (qt_quant_fused)
         y, lctx = qlinear.forward(x2, w.detach(), scheme=scheme, hadamard=hadamard, seed=xi,
                                   out_dtype=x.dtype if x.dtype in (torch.bfloat16, torch.float32) else torch.float32,
-                                  check_finite=False, bwd_xi=int(xi), bwd_rounding=rounding,
-                                  token_offset=shard[0], total_tokens=shard[1])
+                                  check_finite=nonfinite_flag(x.device), bwd_xi=int(xi), bwd_rounding=rounding,
+                                  token_offset=shard[0], total_tokens=shard[1], bwd_xi_dev=xi_dev)
         ctx.lctx = lctx
         ctx.xi = int(xi)
         ctx.rounding = rounding
@@ -49,10 +77,10 @@ class QuartetLinearFn(torch.autograd.Function):
             dy2 = dy2.float()
         dx, dw = qlinear.backward(dy2, ctx.lctx, ctx.xi, ctx.rounding, dx_dtype=ctx.x_dtype
                                   if ctx.x_dtype in (torch.bfloat16, torch.float32) else torch.float32,
-                                  dw_dtype=torch.float32, check_finite=False, token_offset=ctx.shard[0],
+                                  dw_dtype=torch.float32, check_finite=nonfinite_flag(dy.device), token_offset=ctx.shard[0],
                                   total_tokens=ctx.shard[1])
         ctx.lctx = None
-        return dx.reshape(ctx.x_shape), dw.to(ctx.w_dtype), None, None, None, None, None
+        return dx.reshape(ctx.x_shape), dw.to(ctx.w_dtype), None, None, None, None, None, None
 
 
 class QuartetLinearGroupFn(torch.autograd.Function):
@@ -62,19 +90,19 @@ class QuartetLinearGroupFn(torch.autograd.Function):
     Outputs and weight gradients are bit-identical to separate QuartetLinearFn calls."""
 
     @staticmethod
-    def forward(ctx, x, xis, rounding, hadamard, scheme, shard, *ws):
+    def forward(ctx, x, xis, rounding, hadamard, scheme, shard, xi_devs, *ws):
         lead = x.shape[:-1]
         x2 = x.reshape(-1, x.shape[-1])
         if x2.dtype not in (torch.bfloat16, torch.float32):
             x2 = x2.float()
         ctx.shard = shard
-        x_q = qlinear.quantize_operand(x2, scheme, hadamard)
+        x_q = qlinear.quantize_operand(x2, scheme, hadamard, err=nonfinite_flag(x.device))
         out_dtype = x.dtype if x.dtype in (torch.bfloat16, torch.float32) else torch.float32
         ys, ctx.lctxs = [], []
-        for w, xi in zip(ws, xis):
+        for w, xi, xd in zip(ws, xis, xi_devs):
             y, lctx = qlinear.forward(x2, w.detach(), scheme=scheme, hadamard=hadamard, out_dtype=out_dtype,
-                                      check_finite=False, bwd_xi=int(xi), bwd_rounding=rounding,
-                                      token_offset=shard[0], total_tokens=shard[1], x_q=x_q)
+                                      check_finite=nonfinite_flag(x.device), bwd_xi=int(xi), bwd_rounding=rounding,
+                                      token_offset=shard[0], total_tokens=shard[1], x_q=x_q, bwd_xi_dev=xd)
             ys.append(y.reshape(*lead, w.shape[0]))
             ctx.lctxs.append(lctx)
         ctx.xis, ctx.rounding, ctx.x_shape, ctx.x_dtype = [int(v) for v in xis], rounding, x.shape, x.dtype
@@ -92,12 +120,12 @@ class QuartetLinearGroupFn(torch.autograd.Function):
             # the layers' dx are summed in x's dtype (as autograd would accumulate them) by the dx GEMM's
             # epilogue adding into the first layer's dx (QT_EPI_ACCUMULATE): no separate add pass
             dx_sum, dw = qlinear.backward(dy2.contiguous(), lctx, xi, ctx.rounding, dx_dtype=dx_dtype,
-                                          dw_dtype=torch.float32, check_finite=False,
+                                          dw_dtype=torch.float32, check_finite=nonfinite_flag(dy2.device),
                                           token_offset=ctx.shard[0], total_tokens=ctx.shard[1],
                                           dx_accumulate=dx_sum)
             dws.append(dw.to(wdt))
         ctx.lctxs = None
-        return (dx_sum.reshape(ctx.x_shape), None, None, None, None, None, *dws)
+        return (dx_sum.reshape(ctx.x_shape), None, None, None, None, None, None, *dws)
 
 
 def quartet_linear_group(x, mods):
@@ -113,7 +141,7 @@ def quartet_linear_group(x, mods):
         if m.training:
             m.step += 1
     return QuartetLinearGroupFn.apply(x, xis, m0.rounding, m0.hadamard, m0.scheme, m0.token_shard,
-                                      *[m.weight for m in mods])
+                                      [m.xi_slot for m in mods], *[m.weight for m in mods])
 
 
 def quartet_linear(x, w, xi: int, rounding: str = "rtn", hadamard: bool = True,
@@ -147,16 +175,22 @@ class QuartetLinear(torch.nn.Module):
         self.rounding, self.hadamard, self.scheme = rounding, hadamard, scheme
         self.step = 0
         self.token_shard: tuple = (0, None)   # (token offset, global tokens) of this rank: set_token_shard
+        # (uint64 device tensor, index): the backward seed of the current step lives on the device (a training step
+        # captured as one CUDA graph, llama.LlamaQuartet.use_device_seeds); xi() is then a placeholder
+        self.xi_slot = None
         torch.nn.init.normal_(self.weight, std=1.0 / math.sqrt(in_features))
 
     def xi(self) -> int:
+        if self.xi_slot is not None:
+            return DEVICE_XI
         return derive_seed(derive_seed(self.seed, 4, self.step), self.layer_id)
 
     def forward(self, x):
         xi = self.xi()
         if self.training:
             self.step += 1
-        return QuartetLinearFn.apply(x, self.weight, xi, self.rounding, self.hadamard, self.scheme, self.token_shard)
+        return QuartetLinearFn.apply(x, self.weight, xi, self.rounding, self.hadamard, self.scheme, self.token_shard,
+                                     self.xi_slot)
 
     def extra_repr(self) -> str:
         return (f"in_features={self.in_features}, out_features={self.out_features}, "

@@ -29,7 +29,7 @@ import torch
 
 from . import _lib
 from .mxfp4 import (GROUP, MXOperand, derive_seed, gemm, quant_cols, quant_dual, quant_fused, quant_rows, sign_bits,
-                    sign_bits_pair)
+                    sign_bits_pair, sign_bits_pair_dev)
 
 PRE_SCALE = 0.75                     # qlinear.py:36
 POST_SCALE = 16.0 / 9.0              # qlinear.py:37
@@ -144,8 +144,17 @@ def _err_flag(device) -> torch.Tensor:
     return torch.zeros(1, dtype=torch.int32, device=device)
 
 
-def _raise_if_nonfinite(err: torch.Tensor | None) -> None:
-    if err is not None and int(err.item()) != 0:
+def _err_for(check_finite, device):
+    """check_finite: True -> a fresh device flag, checked (one host sync) before returning; False -> no check;
+    a device int32 tensor -> OR the quantizers' non-finite bit into it and return without syncing (the caller
+    checks once later, e.g. nn.raise_if_nonfinite at the end of a training step)."""
+    if isinstance(check_finite, torch.Tensor):
+        return check_finite
+    return _err_flag(device) if check_finite else None
+
+
+def _raise_if_nonfinite(err: torch.Tensor | None, check_finite=True) -> None:
+    if err is not None and not isinstance(check_finite, torch.Tensor) and int(err.item()) != 0:
         raise ValueError("non-finite input")
 
 
@@ -168,7 +177,7 @@ def quantize_operand(m: torch.Tensor, scheme: QuantScheme, hadamard: bool, seed:
 def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, policy: GemmPolicy = DEFAULT_POLICY,
             hadamard: bool = True, seed: int | None = None, out_dtype: torch.dtype = torch.float32,
             check_finite: bool = True, bwd_xi: int | None = None, bwd_rounding: str = "rtn", token_offset: int = 0,
-            total_tokens: int | None = None, x_q: MXOperand | None = None):
+            total_tokens: int | None = None, x_q: MXOperand | None = None, bwd_xi_dev: tuple | None = None):
     """y = x @ w.T through the quantized pipeline; returns (y, context)  (qlinear.py:114-165).
 
     ``x_q``: the forward operand of x (``quantize_operand(x, ...)``) when several layers read the same x
@@ -197,21 +206,30 @@ def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, polic
             raise ValueError("sr_absmax forward requires a seed")
         sx = derive_seed(seed, _TAG_FWD_X)
         sw = derive_seed(seed, _TAG_FWD_W)
-    err = _err_flag(x.device) if check_finite else None
+    err = _err_for(check_finite, x.device)
     eager = None
     if x_q is not None and (x_q.rows != batch or x_q.cols != d_in):
         raise ValueError("shared x_q does not match x")
-    if bwd_xi is not None and bwd_rounding in ("rtn", "sr") and batch % g == 0 and d_out % g == 0:
+    if bwd_xi_dev is not None and (bwd_xi is None or batch % g or d_out % g or scheme.kind == "sr_absmax"):
+        raise NotImplementedError("device-resident seeds need bwd_xi, 32-multiple batch / d_out and a QuEST or RTN "
+                                  "forward scheme")
+    if bwd_xi is not None and bwd_rounding in ("rtn", "sr", "sr_fast") and batch % g == 0 and d_out % g == 0:
         total = batch if total_tokens is None else int(total_tokens)
         if token_offset % g or token_offset < 0 or token_offset + batch > total:
             raise ValueError(f"token shard [{token_offset}, +{batch}) invalid for {total} tokens (block {g})")
         rc = _rounding_code(bwd_rounding)
-        sr = bwd_rounding == "sr"
+        sr = bwd_rounding in ("sr", "sr_fast")
         row_rc = {"quest": _lib.QT_ROUND_QUEST, "rtn_absmax": _lib.QT_ROUND_RTN, "sr_absmax": _lib.QT_ROUND_SR}[scheme.kind]
         fwd_t = _lib.QT_TRANSFORM_HADAMARD if hadamard else _lib.QT_TRANSFORM_NONE
         bwd_t = _lib.QT_TRANSFORM_RANDOMIZED if hadamard else _lib.QT_TRANSFORM_NONE
-        d_signs, t_signs = (sign_bits_pair(bwd_xi, d_out, batch, x.device, start_b=token_offset) if hadamard
-                            else (None, None))
+        if bwd_xi_dev is not None and sr:
+            raise NotImplementedError("device-resident seeds (captured training steps) support rounding='rtn'")
+        if not hadamard:
+            d_signs, t_signs = None, None
+        elif bwd_xi_dev is not None:   # the step's seed lives on the device (a captured training step)
+            d_signs, t_signs = sign_bits_pair_dev(bwd_xi_dev, d_out, batch, x.device, start_b=token_offset)
+        else:
+            d_signs, t_signs = sign_bits_pair(bwd_xi, d_out, batch, x.device, start_b=token_offset)
         x_seed = derive_seed(bwd_xi, _TAG_BWD_X) if sr else 0
         if x_q is None:
             x_q, xt_q = quant_fused(x, row_rc, rc, transform=fwd_t, col_transform=bwd_t, col_signs=t_signs,
@@ -231,7 +249,7 @@ def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, polic
             x_q = quantize_operand(x, scheme, hadamard, sx, err, row_offset=token_offset)
         w_q = quantize_operand(w, scheme, hadamard, sw, err)
     y = gemm(x_q, w_q, out_dtype=out_dtype)
-    _raise_if_nonfinite(err)
+    _raise_if_nonfinite(err, check_finite)
     ctx = LayerContext(x_q=x_q, w_q=w_q, scheme=scheme, policy=policy, hadamard=hadamard,
                        batch=batch, d_in=d_in, d_out=d_out, eager=eager)
     return y, ctx
@@ -248,6 +266,8 @@ def _rounding_code(rounding: str) -> int:
         return _lib.QT_ROUND_RTN
     if rounding == "sr":
         return _lib.QT_ROUND_SR
+    if rounding == "sr_fast":   # B200 extension: unbiased SR with hash uniforms (not the reference's draws)
+        return _lib.QT_ROUND_SR_FAST
     if rounding == "exact":
         raise NotImplementedError("rounding='exact' skips quantization: a CPU test mode (oracle), not a GPU path")
     raise ValueError(f"unknown backward rounding {rounding!r}")
@@ -274,7 +294,7 @@ def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn"
     hadamard=False (the reference checks them only for hadamard=True and quantizes a ragged trailing
     group).  They are the contraction axes of the dx / dw GEMMs, whose MXFP4 operands are whole
     32-element blocks; ragged shapes raise ValueError here (INTEGRATION.md lists the rejected cases)."""
-    if rounding not in ("exact", "rtn", "sr"):
+    if rounding not in ("exact", "rtn", "sr", "sr_fast"):
         raise ValueError(f"unknown backward rounding {rounding!r}")
     rc = _rounding_code(rounding)
     _check_out_dtype("dw_dtype", dw_dtype)
@@ -301,8 +321,8 @@ def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn"
         # along d_out and along tokens, one launch
         d_signs, t_signs = (sign_bits_pair(xi, ctx.d_out, ctx.batch, dev, start_b=token_offset) if ctx.hadamard
                             else (None, None))
-    sr = rounding == "sr"
-    err = _err_flag(dev) if check_finite else None
+    sr = rounding in ("sr", "sr_fast")
+    err = _err_for(check_finite, dev)
 
     # both dy operands from one read of dy: G (rows, qlinear.py:214) and G_t (cols, qlinear.py:234)
     g_q, gt_q = quant_dual(dy, rc, transform=transform, signs=d_signs, col_signs=t_signs, prescale=PRE_SCALE,
@@ -324,7 +344,7 @@ def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn"
                                                      sr_seed=derive_seed(xi, _TAG_BWD_X) if sr else 0,
                                                      counter_start=token_offset, counter_ld=total, err=err)
     dw = gemm(gt_q, xt_q, out_dtype=dw_dtype, mask=ctx.w_q.mask, hadamard=ctx.hadamard, scale=_POST_F32)
-    _raise_if_nonfinite(err)
+    _raise_if_nonfinite(err, check_finite)
     if return_operands:
         return dx, dw, {"g_q": g_q, "wt_q": wt_q, "gt_q": gt_q, "xt_q": xt_q}
     return dx, dw

@@ -64,9 +64,11 @@ def test_row_sums_are_numpy_pairwise():
         assert np.array_equal(seam_row_sums(ta, None, 1).cpu().numpy(), (a * a).sum(axis=1)), n
 
 
-def test_production_sr_unbiased_zscores(diag):
+@pytest.mark.parametrize("mode", ["sr", "sr_fast"])
+def test_production_sr_unbiased_zscores(diag, mode):
     """selftest.py:125-153 (c04) on the tiled SR kernel: 100 fp32 inputs of 32 elements at scales
-    2^-4 .. 2^4, 1e5 draws each (distinct stream positions), z of the mean against the input."""
+    2^-4 .. 2^4, 1e5 draws each (distinct stream positions), z of the mean against the input.  "sr" is the
+    reference's splitmix64 stream, "sr_fast" the hash-uniform mode (QT_ROUND_SR_FAST)."""
     import torch
 
     from paper_2505_14669_b200 import _lib
@@ -78,7 +80,8 @@ def test_production_sr_unbiased_zscores(diag):
         base = diag.gaussians(derive_seed(seed, 4, i), 0x4755, 0, width) * 2.0 ** ((i % 9) - 4)
         b32 = torch.from_numpy(base.astype(np.float32)).cuda()
         x = b32.view(1, width).expand(draws, width).contiguous()
-        op = quant_rows(x, _lib.QT_TRANSFORM_NONE, _lib.QT_ROUND_SR, sr_seed=derive_seed(seed, 4, i, 1))
+        rc = _lib.QT_ROUND_SR if mode == "sr" else _lib.QT_ROUND_SR_FAST
+        op = quant_rows(x, _lib.QT_TRANSFORM_NONE, rc, sr_seed=derive_seed(seed, 4, i, 1))
         d = op.dequantize(torch.float64)
         mean = d.mean(dim=0)
         se = d.std(dim=0) / draws ** 0.5
@@ -87,3 +90,25 @@ def test_production_sr_unbiased_zscores(diag):
     zs = np.concatenate(zs)
     frac3, zmax = float((zs > 3.0).mean()), float(zs.max())
     assert frac3 <= 0.01 and zmax <= 6.0, (frac3, zmax)
+
+
+def test_sr_fast_rounds_to_the_same_neighbours():
+    """QT_ROUND_SR_FAST draws differ from the reference's stream, but every code is one of the two grid
+    neighbours the exact SR picks from and the E8M0 scales are identical."""
+    import torch
+
+    from paper_2505_14669_b200 import _lib
+    from paper_2505_14669_b200.mxfp4 import quant_rows
+
+    g = torch.Generator(device="cuda").manual_seed(4)
+    x = torch.randn(512, 1024, device="cuda", generator=g) * torch.exp2(torch.randint(-8, 8, (512, 1), device="cuda",
+                                                                                        generator=g).float())
+    a = quant_rows(x, _lib.QT_TRANSFORM_HADAMARD, _lib.QT_ROUND_SR, sr_seed=77)
+    b = quant_rows(x, _lib.QT_TRANSFORM_HADAMARD, _lib.QT_ROUND_SR_FAST, sr_seed=77)
+    assert torch.equal(a.scales_rowmajor(), b.scales_rowmajor())
+    da, db = a.dequantize(torch.float64), b.dequantize(torch.float64)
+    step = torch.exp2(a.scales_rowmajor().double() - 127).repeat_interleave(32, dim=1) * 2.0   # widest grid gap
+    assert bool(((da - db).abs() <= step).all())
+    assert not torch.equal(a.codes, b.codes)       # a different (hash) stream
+    c = quant_rows(x, _lib.QT_TRANSFORM_HADAMARD, _lib.QT_ROUND_SR_FAST, sr_seed=77)
+    assert torch.equal(b.codes, c.codes)           # deterministic given the seed

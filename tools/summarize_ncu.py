@@ -2,11 +2,12 @@
 import csv
 import io
 import json
+import os
 import subprocess
 import sys
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
-out_dir = "profiles"
+out_dir = os.environ.get("OUT_DIR", "profiles")
 
 # ---- launch list (cold-cache, serialised): shares per kernel family for the second (steady) step
 rows = list(csv.reader(open(f"gpurun_out/launches_{tag}.csv")))
@@ -19,7 +20,8 @@ step = launches[half:]  # second iteration of the 3-shape step
 fam = {}
 for _, name, ns in step:
     key = name.split("(")[0].replace("void ", "")
-    key = ("k_gemm_mxf4" if "k_gemm" in key else "k_tcq_dual" if "k_tcq" in key else
+    key = ("k_gemm_mxf4" if "k_gemm" in key else "k_tcq_dual" if "k_tcq_dual" in key else
+           "k_tcq_xq" if "k_tcq_xq" in key else
            "k_quant" if "k_quant" in key else "k_signs" if "k_signs" in key else "torch/other")
     fam[key] = fam.get(key, 0.0) + ns
 total = sum(fam.values())

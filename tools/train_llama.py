@@ -41,9 +41,12 @@ def main():
         dist.destroy_process_group()
 
 
-def run(llama, preset, batch, steps, warmup, block, dev, world=1, rank=0, linear="quartet"):
+def run(llama, preset, batch, steps, warmup, block, dev, world=1, rank=0, linear="quartet", graph=None):
     """linear: "quartet" (every linear MXFP4 through libquartet_b200) or "bf16" (the comparator arm: the
-    same model, glue kernels, optimizer and data with bf16 cuBLAS linears)."""
+    same model, glue kernels, optimizer and data with bf16 cuBLAS linears).  graph (default: one GPU): the
+    training step is captured once as a CUDA graph and replayed (Trainer(graph=True)); both arms alike."""
+    if graph is None:
+        graph = world == 1
     import torch
     import torch.distributed as dist
 
@@ -61,7 +64,7 @@ def run(llama, preset, batch, steps, warmup, block, dev, world=1, rank=0, linear
             y.float().square().mean().backward()
             return None
     else:
-        tr = llama.Trainer(model, steps=1000, lr=llama.PAPER_LR[preset])
+        tr = llama.Trainer(model, steps=1000, lr=llama.PAPER_LR[preset], graph=graph)
         tok, tgt = llama.synthetic_batch(cfg, batch, seed=rank, device=dev)
 
         def step(i):
@@ -84,6 +87,7 @@ def run(llama, preset, batch, steps, warmup, block, dev, world=1, rank=0, linear
         ms = float(t.item())
     lin = cfg.n_layer * (4 * cfg.d_model ** 2 + 3 * cfg.d_model * cfg.hidden) + (0 if block else cfg.d_model * cfg.vocab)
     out = {"preset": preset, "linear": linear, "block_only": block, "n_layer": cfg.n_layer, "d_model": cfg.d_model,
+           "launch": "eager" if block or not graph else "CUDA graph of the whole training step",
            "seq_len": cfg.seq_len, "seqs_per_gpu": batch, "n_gpus": world, "ms_per_step": round(ms, 3),
            "tokens_per_s": round(world * tokens / (ms * 1e-3), 1),
            "linear_tflops": round(world * 6 * tokens * lin / (ms * 1e-3) / 1e12, 1)}
