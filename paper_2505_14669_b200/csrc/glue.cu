@@ -211,6 +211,7 @@ __global__ void k_xent(const uint4* __restrict__ logits, const int64_t* __restri
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
         const uint4* row = logits + r * V8;
         const int64_t t = tgt[r];
+        const bool valid = t >= 0 && t < V;   // otherwise ignored (loss 0, gradient 0), like ignore_index
         if (!backward) {
             float m = -INFINITY, sum = 0.f;
             for (int i = threadIdx.x; i < V8; i += blockDim.x) {
@@ -243,12 +244,16 @@ __global__ void k_xent(const uint4* __restrict__ logits, const int64_t* __restri
                 for (int k = 1; k < nw; ++k) ce_merge(M, S, sm[k], ss[k]);
                 const float l = M + __logf(S);
                 lse[r] = l;
-                const uint32_t tw = reinterpret_cast<const uint32_t*>(row)[t >> 1];
-                loss[r] = l - bf(tw, (int)(t & 1));
+                if (valid) {
+                    const uint32_t tw = reinterpret_cast<const uint32_t*>(row)[t >> 1];
+                    loss[r] = l - bf(tw, (int)(t & 1));
+                } else {
+                    loss[r] = 0.f;
+                }
             }
             __syncthreads();
         } else {
-            const float l = lse[r], g = *dloss * scale;
+            const float l = lse[r], g = valid ? *dloss * scale : 0.f;
             uint4* drow = dlogits + r * V8;
             for (int i = threadIdx.x; i < V8; i += blockDim.x) {
                 const uint4 c = row[i];

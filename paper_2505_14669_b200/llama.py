@@ -174,17 +174,20 @@ class _CrossEntropy(torch.autograd.Function):
         _lib.check(_lib.load().qt_cross_entropy(logits.data_ptr(), targets.data_ptr(), rows, vocab, lse.data_ptr(),
                                                 loss.data_ptr(), None, None, 1.0, 0, _stream(logits.device)),
                    "qt_cross_entropy")
-        ctx.save_for_backward(logits, targets, lse)
-        return loss.mean()
+        # targets outside [0, vocab) (e.g. ignore_index = -100) contribute nothing and are not counted, as in
+        # F.cross_entropy's mean reduction; the count stays on the device (no sync)
+        n_valid = ((targets >= 0) & (targets < vocab)).sum().to(torch.float32)
+        ctx.save_for_backward(logits, targets, lse, n_valid)
+        return loss.sum() / n_valid
 
     @staticmethod
     def backward(ctx, g):
-        logits, targets, lse = ctx.saved_tensors
+        logits, targets, lse, n_valid = ctx.saved_tensors
         rows, vocab = logits.shape
-        g = g.detach().to(torch.float32).contiguous()
+        g = (g.detach().to(torch.float32) / n_valid).reshape(1).contiguous()
         d = torch.empty_like(logits)
         _lib.check(_lib.load().qt_cross_entropy(logits.data_ptr(), targets.data_ptr(), rows, vocab, lse.data_ptr(),
-                                                None, d.data_ptr(), g.data_ptr(), 1.0 / rows, 1,
+                                                None, d.data_ptr(), g.data_ptr(), 1.0, 1,
                                                 _stream(logits.device)), "qt_cross_entropy")
         return d, None
 

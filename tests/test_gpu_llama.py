@@ -111,11 +111,15 @@ def test_fused_rmsnorm_matches_fp32_reference(llama, d):
     torch.testing.assert_close(dw, dwf, rtol=1e-4, atol=1e-3)
 
 
-def test_fused_cross_entropy_matches_fp32_reference(llama):
-    """csrc/glue.cu cross-entropy (loss and dlogits) vs torch's fp32 cross-entropy on the same bf16 logits."""
+@pytest.mark.parametrize("ignore", [False, True])
+def test_fused_cross_entropy_matches_fp32_reference(llama, ignore):
+    """csrc/glue.cu cross-entropy (loss and dlogits) vs torch's fp32 cross-entropy on the same bf16 logits;
+    with ignore, some targets are -100 (torch's ignore_index): no loss, no gradient, not counted."""
     g = torch.Generator(device="cuda").manual_seed(5)
     logits = (torch.randn(300, 4000, device="cuda", generator=g) * 3).to(torch.bfloat16).requires_grad_(True)
     tgt = torch.randint(0, 4000, (300,), device="cuda", generator=g)
+    if ignore:
+        tgt[::7] = -100
     loss = llama.cross_entropy(logits, tgt)
     lf = logits.detach().float().requires_grad_(True)
     ref = torch.nn.functional.cross_entropy(lf, tgt)
