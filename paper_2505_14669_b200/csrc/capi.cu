@@ -213,11 +213,12 @@ int qt_quant_dual(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64_
                 col_counter_ld, rounding == QT_ROUND_SR_FAST};
     QuantOut ro{row_codes, row_ldc, row_sf, row_katoms, row_mask, err, nullptr};
     QuantOut co{col_codes, col_ldc, col_sf, col_katoms, nullptr, err, nullptr};
-    if (g_quant_mode == 0 && in_dtype == QT_IN_BF16 && rounding == QT_ROUND_RTN &&
+    if (g_quant_mode != 1 && in_dtype == QT_IN_BF16 && (rounding == QT_ROUND_RTN || rounding == QT_ROUND_SR_FAST) &&
         transform == QT_TRANSFORM_RANDOMIZED && !row_mask) {
-        // tensor-core Hadamard + checked RTN (bit-identical; exact CUDA-core fallback per group)
+        // tensor-core Hadamard + checked RTN (bit-identical; exact fallback per group) or fast SR
+        const bool srf = rounding == QT_ROUND_SR_FAST;
         int rc2 = launch_tcq_dual(x, ldx, rows, cols, row_sign_bits, col_sign_bits, prescale, ro, co,
-                                  g_quant_fallbacks, (cudaStream_t)stream);
+                                  g_quant_fallbacks, (cudaStream_t)stream, srf ? &rc : nullptr, srf ? &cc : nullptr);
         return rc2 == 1001 || rc2 == 1002 ? QT_ERR_TMA : rc2;
     }
     MxIn mx{nullptr, 0, nullptr, 0};
@@ -249,11 +250,11 @@ int qt_quant_fused(const void* x, int in_dtype, int64_t ldx, int64_t rows, int64
     QuantOut ro{row_codes, row_ldc, row_sf, row_katoms, row_mask, err, fallbacks};
     QuantOut co{col_codes, col_ldc, col_sf, col_katoms, nullptr, err, nullptr};
     if (g_quant_mode != 1 && in_dtype == QT_IN_BF16 && row_rounding == QT_ROUND_QUEST &&
-        row_transform == QT_TRANSFORM_HADAMARD && row_prescale == 1.0f && col_rounding == QT_ROUND_RTN &&
-        col_transform == QT_TRANSFORM_RANDOMIZED) {
-        // X_q and X_t both on the tensor cores (checked QuEST / RTN, exact per-group fallback)
+        row_transform == QT_TRANSFORM_HADAMARD && row_prescale == 1.0f &&
+        (col_rounding == QT_ROUND_RTN || col_rounding == QT_ROUND_SR_FAST) && col_transform == QT_TRANSFORM_RANDOMIZED) {
+        // X_q and X_t both on the tensor cores (checked QuEST / RTN, exact per-group fallback; or fast-SR X_t)
         int rc3 = launch_tcq_xq(x, ldx, rows, cols, ro, col_sign_bits, col_prescale, co, g_quant_fallbacks,
-                                (cudaStream_t)stream);
+                                (cudaStream_t)stream, col_rounding == QT_ROUND_SR_FAST ? &cc : nullptr);
         return rc3 == 1001 || rc3 == 1002 ? QT_ERR_TMA : rc3;
     }
     MxIn mx{nullptr, 0, nullptr, 0};

@@ -47,18 +47,12 @@ __device__ __forceinline__ float exp2i(int e) {  // 2^e as fp32, e in [-149, 127
 
 // E2M1 encode of two fp32 values with RNE + satfinite (ties-to-even-mantissa, clamp at 6):
 // identical to the reference's midpoint ladder (_numpy.py:26-40).  Returns the byte with `lo`
-// in the low nibble.  Negative zero is NOT canonicalised here (see canon_nz).
+// in the low nibble.  Negative zero is NOT canonicalised here (see canon8 in qgroup.cuh).
 __device__ __forceinline__ uint32_t e2m1x2(float lo, float hi) {
     uint16_t r;
     asm("{\n .reg .b8 t;\n cvt.rn.satfinite.e2m1x2.f32 t, %1, %2;\n cvt.u16.u8 %0, t;\n}"
         : "=h"(r) : "f"(hi), "f"(lo));
     return r;
-}
-// Reference canonicalises -0 to +0 (codec.py:11, _native.pyx:127-130): clear the sign of every
-// nibble whose magnitude bits are zero.
-__device__ __forceinline__ uint32_t canon_nz(uint32_t c) {
-    uint32_t keep = ((c & 0x77777777u) + 0x77777777u) & 0x88888888u;
-    return (c & 0x77777777u) | (c & keep);
 }
 // Decode an E2M1 byte pair to fp32 (exact).
 __device__ __forceinline__ float2 e2m1x2_to_f32(uint32_t byte) {

@@ -76,11 +76,13 @@ int launch_quant_tile(const void* x, int in_type, int64_t ldx, const MxIn& mx, i
                       const QuantOut* col_out, int col_from_codes, cudaStream_t st);
 int launch_tcq_xq(const void* x, int64_t ldx, int64_t R, int64_t C, const QuantOut& row_out,
                   const uint32_t* col_sign_bits, float col_prescale, const QuantOut& col_out, int* fallbacks,
-                  cudaStream_t st);
+                  cudaStream_t st, const QuantCfg* srf_col = nullptr);   // srf_col: X_t by QT_ROUND_SR_FAST
 extern int g_tcq_dbg;  // experiment knobs of the tensor-core quantizer (0 in production)
+// srf_row / srf_col (both or neither): QT_ROUND_SR_FAST with these keys / stream layouts instead of RTN
 int launch_tcq_dual(const void* x, int64_t ldx, int64_t R, int64_t C, const uint32_t* row_sign_bits,
                     const uint32_t* col_sign_bits, float prescale, const QuantOut& row_out, const QuantOut& col_out,
-                    int* fallbacks, cudaStream_t st);
+                    int* fallbacks, cudaStream_t st, const QuantCfg* srf_row = nullptr,
+                    const QuantCfg* srf_col = nullptr);
 extern int g_gemm_2sm;
 extern int g_gemm_cluster8;
 int launch_gemm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, int64_t a_katoms, const uint8_t* b, int64_t ldb,

@@ -129,31 +129,17 @@ __device__ __forceinline__ uint32_t sr_code(float x, float sc_f, double sc_d, ui
 }
 
 
-// Fast stochastic rounding (B200 extension, QT_ROUND_SR_FAST; SURVEY.md section 7.3 "fast mode"): the same
-// signed-grid neighbours and the same p = (v - lo) / (hi - lo) as sr_code -- computed in fp32, where it is
-// exact (v - lo is exact by Sterbenz, v and lo lie within a factor 2, and the span is a power of two) --
-// against a 24-bit uniform from a 32-bit hash of (key, stream position) instead of the reference's splitmix64
-// 53-bit uniform.  E[code value] = lo + ceil(p 2^24) 2^-24 (hi - lo): unbiased up to 2^-24 of a grid step;
-// the draws are NOT the reference's.  ~25 instructions per element less than sr_code (no 64-bit multiplies,
-// no f64).
-__device__ __forceinline__ uint32_t sr_code_fast(float x, float sc_f, uint32_t k0, uint32_t k1, uint64_t index) {
-    const float a = fabsf(x) * sc_f;
-    int b;
-    float lo;
-    uint32_t c_lo, c_hi;
-    if (x > 0.0f) {
-        b = (a > 0.5f) + (a > 1.0f) + (a > 1.5f) + (a > 2.0f) + (a > 3.0f) + (a > 4.0f);
-        lo = b <= 4 ? 0.5f * b : (float)(b - 2);
-        c_lo = (uint32_t)b;
-        c_hi = (uint32_t)(b + 1);
-    } else {
-        b = (a >= 0.5f) + (a >= 1.0f) + (a >= 1.5f) + (a >= 2.0f) + (a >= 3.0f) + (a >= 4.0f);
-        lo = -(b + 1 <= 4 ? 0.5f * (b + 1) : (b + 1 == 7 ? 6.0f : (float)(b - 1)));
-        c_lo = 8u | (uint32_t)(b + 1);
-        c_hi = b == 0 ? 0u : (8u | (uint32_t)b);
-    }
-    const float inv_span = b < 4 ? 2.0f : (b < 6 ? 1.0f : 0.5f);
-    const float p = __fmul_rn(__fsub_rn(__fmul_rn(x, sc_f), lo), inv_span);
+// Fast stochastic rounding (B200 extension, QT_ROUND_SR_FAST; SURVEY.md section 7.3 "fast mode"): the same two
+// grid neighbours as sr_code, picked with the same probability (up to 2^-22 of a grid step), from a 32-bit hash
+// of (key, stream position) instead of the reference's splitmix64 stream -- the draws are NOT the reference's.
+// No 64-bit multiplies, no f64, no neighbour ladder.
+// The fast-SR code of an already scaled value v (= x / s, |v| <= 6).  On [0.5, 8) the E2M1 grid keeps 1 mantissa
+// bit (0 on [0.5, 1)), so stochastic rounding is "add a uniform integer below the dropped bits, then truncate":
+// the result is the upper neighbour with probability (dropped bits) / 2^drop = (|v| - lo) / (hi - lo), and a carry
+// lands exactly on the next grid point.  Below 0.5 the neighbours are 0 and 0.5 with P(0.5) = 2 |v| (24-bit
+// uniform).  The sign is applied to the magnitude's code (the grid is symmetric, so the distribution equals the
+// reference's signed-grid SR).  Uniforms from a 32-bit hash of (key, stream position).
+__device__ __forceinline__ uint32_t sr_fast_code(float v, uint32_t k0, uint32_t k1, uint64_t index) {
     uint32_t h = (uint32_t)index * 0x9E3779B1u + k0;          // lowbias32 of (position, key)
     h ^= (uint32_t)(index >> 32) * 0x85EBCA77u + k1;
     h ^= h >> 16;
@@ -161,6 +147,18 @@ __device__ __forceinline__ uint32_t sr_code_fast(float x, float sc_f, uint32_t k
     h ^= h >> 15;
     h *= 0x846CA68Bu;
     h ^= h >> 16;
-    return (float)(h >> 8) < __fmul_rn(p, 16777216.0f) ? c_hi : c_lo;
+    const uint32_t bits = __float_as_uint(v) & 0x7FFFFFFFu;
+    uint32_t mag;
+    if (bits >= 0x3F000000u) {                                // |v| >= 0.5
+        const uint32_t mask = bits >= 0x3F800000u ? 0x3FFFFFu : 0x7FFFFFu;
+        mag = (bits + ((h >> 9) & mask)) & ~mask;
+    } else {
+        mag = (float)(h >> 8) < __fmul_rn(__uint_as_float(bits), 33554432.0f) ? 0x3F000000u : 0u;
+    }
+    const uint32_t c = e2m1x2(__uint_as_float(mag), 0.0f) & 7u;   // exact grid value -> its magnitude code
+    return c == 0 ? 0u : c | ((__float_as_uint(v) >> 28) & 8u);
+}
+__device__ __forceinline__ uint32_t sr_code_fast(float x, float sc_f, uint32_t k0, uint32_t k1, uint64_t index) {
+    return sr_fast_code(__fmul_rn(x, sc_f), k0, k1, index);
 }
 }  // namespace qt

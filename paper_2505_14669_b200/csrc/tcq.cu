@@ -50,6 +50,11 @@ struct TqArgs {
     float prescale;
     int* fallbacks;              // nullable: groups recomputed exactly
     int dbg;                     // experiment knobs (0 in production): 1 skip quantize, 2 skip B build, 4 skip TMEM ld, 8 skip stores
+    // QT_ROUND_SR_FAST (srf != 0): keys and stream layout of the two operands (qt_quant_dual's positions:
+    // G r*ld_r + c from ctr_r, G_t c*ld_c + r from ctr_c)
+    int srf;
+    uint64_t key_r, key_c, ctr_r, ctr_c;
+    int64_t ld_r, ld_c;
 };
 
 // Four of the 1024 16-byte chunks of a tile's 8 signed Hadamard blocks (4 row-pass blocks from the column
@@ -76,6 +81,7 @@ __device__ __forceinline__ void build_b_chunks(uint32_t Bs, const uint8_t* lut, 
     }
 }
 
+template <bool SRF>   // SRF: QT_ROUND_SR_FAST codes instead of checked RTN (its own instantiation: no cost for RTN)
 __global__ void __launch_bounds__(kTqThreads, 1)
     k_tcq_dual(const __grid_constant__ CUtensorMap tmX, TqArgs a) {
     extern __shared__ uint8_t smem_raw[];
@@ -213,11 +219,21 @@ __global__ void __launch_bounds__(kTqThreads, 1)
                 }
                 uint4 c0d, c1d;
                 int e0, e1;
-                const bool ok0 = rtn_checked(v0, a.prescale, c0d, e0);
-                const bool ok1 = rtn_checked(v1, a.prescale, c1d, e1);
                 const QuantOut& out = pass ? a.col_out : a.row_out;
                 const int64_t orow = pass ? c0 + li : r0 + li;           // output row
                 const int64_t kb = pass ? r0 : c0;                      // start of the grouped axis (mult. of 128)
+                const uint64_t key = pass ? a.key_c : a.key_r;
+                const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+                // stream position of element 0 of group g0 of this output row
+                const uint64_t pos0 = (pass ? a.ctr_c : a.ctr_r) + (uint64_t)(orow * (pass ? a.ld_c : a.ld_r) + kb + 32 * g0);
+                bool ok0, ok1;
+                if (SRF) {
+                    ok0 = srf_checked(v0, a.prescale, k0, k1, pos0, c0d, e0);
+                    ok1 = srf_checked(v1, a.prescale, k0, k1, pos0 + 32, c1d, e1);
+                } else {
+                    ok0 = rtn_checked(v0, a.prescale, c0d, e0);
+                    ok1 = rtn_checked(v1, a.prescale, c1d, e1);
+                }
                 const int64_t lim_k = pass ? a.R : a.C;
                 const bool in_row = orow < (pass ? a.C : a.R);
                 // undecided groups (~0.1 %): the whole warp recomputes them exactly, one group at a time
@@ -234,7 +250,9 @@ __global__ void __launch_bounds__(kTqThreads, 1)
                             todo &= todo - 1;
                             uint4 cx;
                             int ex;
-                            exact_group_warp(tile, pass == 1, quad * 32 + f, g0 + u, sw, a.prescale, out.err, cx, ex);
+                            const uint64_t pf = SRF ? __shfl_sync(0xffffffffu, pos0, f) + 32 * u : 0;
+                            exact_group_warp(tile, pass == 1, quad * 32 + f, g0 + u, sw, a.prescale, out.err, cx, ex,
+                                             SRF, k0, k1, pf);
                             if (lane == f) {
                                 if (u) {
                                     c1d = cx;
@@ -284,19 +302,33 @@ int g_tcq_dbg = 0;
 // row_sign_bits: signs of the row operand (indexed by column), col_sign_bits: of the col operand (by row)
 int launch_tcq_dual(const void* x, int64_t ldx, int64_t R, int64_t C, const uint32_t* row_sign_bits,
                     const uint32_t* col_sign_bits, float prescale, const QuantOut& row_out, const QuantOut& col_out,
-                    int* fallbacks, cudaStream_t st) {
+                    int* fallbacks, cudaStream_t st, const QuantCfg* srf_row, const QuantCfg* srf_col) {
     if (R == 0 || C == 0) return 0;
     CUtensorMap m;
     const int rc = tq_map(&m, x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R, C, ldx * 2);
     if (rc) return rc;
     static int attr_set[kMaxDevices];
-    if (first_use_on_device(attr_set))
-        cudaFuncSetAttribute(k_tcq_dual, cudaFuncAttributeMaxDynamicSharedMemorySize, kTqBytes);
+    if (first_use_on_device(attr_set)) {
+        cudaFuncSetAttribute(k_tcq_dual<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTqBytes);
+        cudaFuncSetAttribute(k_tcq_dual<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTqBytes);
+    }
     const int64_t sms = device_sms();
-    TqArgs a{R, C, row_sign_bits, col_sign_bits, row_out, col_out, prescale, fallbacks, g_tcq_dbg};
+    TqArgs a{R, C, row_sign_bits, col_sign_bits, row_out, col_out, prescale, fallbacks, g_tcq_dbg, 0, 0, 0, 0, 0, C, R};
+    if (srf_row && srf_col) {
+        a.srf = 1;
+        a.key_r = srf_row->sr_base;
+        a.key_c = srf_col->sr_base;
+        a.ctr_r = srf_row->counter_start;
+        a.ctr_c = srf_col->counter_start;
+        a.ld_r = srf_row->counter_ld ? srf_row->counter_ld : C;
+        a.ld_c = srf_col->counter_ld ? srf_col->counter_ld : R;
+    }
     const int64_t tiles = ((R + 127) / 128) * ((C + 127) / 128);
     const unsigned grid = (unsigned)cap_grid(tiles < sms ? tiles : sms);
-    k_tcq_dual<<<grid, kTqThreads, kTqBytes, st>>>(m, a);
+    if (a.srf)
+        k_tcq_dual<true><<<grid, kTqThreads, kTqBytes, st>>>(m, a);
+    else
+        k_tcq_dual<false><<<grid, kTqThreads, kTqBytes, st>>>(m, a);
     return (int)cudaGetLastError();
 }
 

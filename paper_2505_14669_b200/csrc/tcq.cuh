@@ -32,6 +32,39 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn) {
            ((uint32_t)(M >> 4) << 24);
 }
 
+// Fast stochastic rounding (QT_ROUND_SR_FAST) of one group from tensor-core sums: the E8M0 exponent is checked like
+// rtn_checked's (false -> caller takes the exact path); the codes are drawn for the tensor-core values themselves
+// (within the bound B of the reference's, ~1e-6 of a grid step: the mode is statistical, not the reference's draws).
+// Element j uses stream position idx0 + j.
+__device__ __forceinline__ bool srf_checked(const float (&acc)[32], float prescale, uint32_t k0, uint32_t k1,
+                                            uint64_t idx0, uint4& codes, int& e_out) {
+    constexpr float kC5 = 0.17677669f;
+    constexpr float kU = 5.9604645e-08f;
+    const float amax = absmax32(acc);
+    bool ok = amax <= 1.0e30f && (amax >= 1.0e-25f || amax == 0.0f);
+    const float nrm = amax * 5.65685463f;
+    const float bnd = 20.0f * kU * kC5 * nrm * 1.001f;
+    const float amp = amax * kC5 * prescale;
+    const float d = bnd * prescale + 4.0f * kU * amp;
+    const uint32_t ab = __float_as_uint(amp);
+    const int e = amax == 0.0f ? 0 : (int)(ab >> 23) - 2 + ((ab & 0x7FFFFFu) > 0x400000u ? 1 : 0);
+    const float s2 = __uint_as_float((uint32_t)(254 - e) << 23);
+    ok = ok && (amax == 0.0f || (__fmul_rd(amp - d, s2) > 3.0f && __fmul_ru(amp + d, s2) < 6.0f));
+    const float sc = kC5 * prescale * s2;
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint32_t acc4 = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            acc4 |= sr_fast_code(__fmul_rn(acc[8 * q + k], sc), k0, k1, idx0 + (uint64_t)(8 * q + k)) << (4 * k);
+        w[q] = acc4;
+    }
+    codes = make_uint4(w[0], w[1], w[2], w[3]);
+    e_out = e;
+    return ok;
+}
+
 // Checked RTN of one group from tensor-core sums acc (= H (s.x), exact up to 8u sum|x|).
 // Returns false when a decision is within the error bound (caller falls back to the exact path).
 __device__ __forceinline__ bool rtn_checked(const float (&acc)[32], float prescale, uint4& codes, int& e_out) {
@@ -89,27 +122,10 @@ __device__ __forceinline__ bool rtn_checked(const float (&acc)[32], float presca
     return ok && diff == 0;
 }
 
-// Exact (v3) path for one group of the staged tile: row group (row r, columns 32g..) or column group
-// (column c, rows 32g..), signs from the global bitmaps, FWHT replaying the reference, RTN.
-static __device__ __noinline__ void exact_group(const uint8_t* tile, bool col, int idx, int g, uint32_t sw,
-                                         float prescale, int* err, uint4& codes, int& e_out) {
-    float v[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-        const int r = col ? g * 32 + j : idx, c = col ? idx : g * 32 + j;
-        const uint16_t h = *reinterpret_cast<const uint16_t*>(tile + tq_off(r, c));
-        v[j] = __uint_as_float(((uint32_t)h << 16) ^ (((sw >> j) & 1u) << 31));
-    }
-    fwht_full(v);
-    QuantCfg cf{};
-    cf.prescale = prescale;
-    uint32_t mask;
-    e_out = quant_group<kRtn>(v, cf, 0, err, nullptr, codes, mask);
-}
-
-// Warp-cooperative version of exact_group for ONE group (all 32 lanes; lane j holds element j): the checked
-// epilogues hand their rare undecided groups to this one at a time instead of running exact_group in a single
-// diverged lane.  Same operations as the scalar path: the butterfly pairs (t, t + h) meet through a shuffle,
+// Exact path for ONE undecided group of the staged bf16 tile, warp-cooperative (all 32 lanes; lane j holds element
+// j): row group (row idx, columns 32g..) or column group (column idx, rows 32g..), signs sw, the reference's FWHT
+// and RTN.  The checked epilogues hand their rare undecided groups to it one at a time instead of running a scalar
+// exact path in a single diverged lane.  Same operations as the scalar path: the butterfly pairs (t, t + h) meet through a shuffle,
 // the lower index stays the minuend; max |v| is order-independent; each lane encodes its own element.
 __device__ __forceinline__ float max_nan2(float a, float b) {
     float r;
@@ -117,7 +133,9 @@ __device__ __forceinline__ float max_nan2(float a, float b) {
     return r;
 }
 __device__ __forceinline__ void exact_group_warp(const uint8_t* tile, bool col, int idx, int g, uint32_t sw,
-                                                 float prescale, int* err, uint4& codes, int& e_out) {
+                                                 float prescale, int* err, uint4& codes, int& e_out,
+                                                 bool srf = false, uint32_t k0 = 0, uint32_t k1 = 0,
+                                                 uint64_t idx0 = 0) {
     const int j = threadIdx.x & 31;
     const int r = col ? g * 32 + j : idx, c = col ? idx : g * 32 + j;
     const uint16_t h16 = *reinterpret_cast<const uint16_t*>(tile + tq_off(r, c));
@@ -133,9 +151,16 @@ __device__ __forceinline__ void exact_group_warp(const uint8_t* tile, bool col, 
     if (!(am <= 3.4028234663852886e38f) && err && j == 0) atomicOr(err, 1);
     int e;
     float sc;
-    if (!rtn_scale(am, prescale, e, sc)) v = __fmul_rn(v, prescale);
-    uint32_t nib = e2m1b(__fmul_rn(v, sc), 0.0f) & 0xFu;
-    if ((nib & 7u) == 0) nib = 0;   // -0 -> +0 (_native.pyx:127-130)
+    uint32_t nib;
+    if (srf) {   // QT_ROUND_SR_FAST: quant_group<kSr>'s order -- pre-scale, ceil exponent of the pre-scaled amax
+        v = __fmul_rn(v, prescale);
+        e = ceil_scale_exp(__fmul_rn(am, prescale));
+        nib = sr_code_fast(v, exp2i(127 - e), k0, k1, idx0 + (uint64_t)j);
+    } else {
+        if (!rtn_scale(am, prescale, e, sc)) v = __fmul_rn(v, prescale);
+        nib = e2m1b(__fmul_rn(v, sc), 0.0f) & 0xFu;
+        if ((nib & 7u) == 0) nib = 0;   // -0 -> +0 (_native.pyx:127-130)
+    }
     uint32_t w[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) w[q] = __reduce_or_sync(0xffffffffu, (j >> 3) == q ? nib << (4 * (j & 7)) : 0u);

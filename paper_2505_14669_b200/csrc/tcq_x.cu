@@ -44,6 +44,9 @@ struct XqArgs {
     int* fallbacks;           // re-decided groups (nullable): [0] X_q search, [1] X_t, [2] X_q codes only
     int dbg;                  // experiment knobs (0 in production): 1 skip QuEST decisions, 2 skip RTN decisions,
                               // 4 exact CUDA-core row phase for every group
+    int srf;                  // X_t by QT_ROUND_SR_FAST: key, stream start and row stride (c * ld + r)
+    uint64_t key, ctr;
+    int64_t ld;
 };
 
 constexpr float kU24 = 5.9604645e-08f;  // 2^-24
@@ -283,6 +286,7 @@ static __device__ XqGroup xq_exact_row_warp(const uint8_t* tile, int r, int g, i
     return o;
 }
 
+template <bool SRF>   // SRF: X_t by QT_ROUND_SR_FAST instead of checked RTN (its own instantiation)
 __global__ void __launch_bounds__(kXqThreads, 1) k_tcq_xq(const __grid_constant__ CUtensorMap tmX, XqArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -480,6 +484,9 @@ __global__ void __launch_bounds__(kXqThreads, 1) k_tcq_xq(const __grid_constant_
                     codes = make_uint4(__float_as_uint(acc[0]), __float_as_uint(acc[9]), __float_as_uint(acc[17]),
                                        __float_as_uint(acc[31]));
                     e = 120;
+                } else if (SRF) {
+                    ok = srf_checked(acc, a.col_prescale, (uint32_t)a.key, (uint32_t)(a.key >> 32),
+                                     a.ctr + (uint64_t)(orow * a.ld + gk), codes, e);
                 } else {
                     ok = rtn_checked(acc, a.col_prescale, codes, e);
                 }
@@ -491,8 +498,10 @@ __global__ void __launch_bounds__(kXqThreads, 1) k_tcq_xq(const __grid_constant_
                         if (a.fallbacks && lane == 0) atomicAdd(a.fallbacks + 1, 1);
                         uint4 cx;
                         int ex;
+                        const int64_t orf = c0 + quad * 32 + f;
                         exact_group_warp(smem + kXqOffDeq + d * kXqDeq, true, quad * 32 + f, g, sw, a.col_prescale,
-                                         a.col_out.err, cx, ex);
+                                         a.col_out.err, cx, ex, SRF, (uint32_t)a.key, (uint32_t)(a.key >> 32),
+                                         a.ctr + (uint64_t)(orf * a.ld + gk));
                         if (lane == f) {
                             codes = cx;
                             e = ex;
@@ -519,18 +528,30 @@ __global__ void __launch_bounds__(kXqThreads, 1) k_tcq_xq(const __grid_constant_
 // requantization, signs along R) in one pass, transforms on the tensor cores.
 int launch_tcq_xq(const void* x, int64_t ldx, int64_t R, int64_t C, const QuantOut& row_out,
                   const uint32_t* col_sign_bits, float col_prescale, const QuantOut& col_out, int* fallbacks,
-                  cudaStream_t st) {
+                  cudaStream_t st, const QuantCfg* srf_col) {
     if (R == 0 || C == 0) return 0;
     CUtensorMap m;
     const int rc = tq_map(&m, x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R, C, ldx * 2);
     if (rc) return rc;
     static int attr_set[kMaxDevices];
-    if (first_use_on_device(attr_set))
-        cudaFuncSetAttribute(k_tcq_xq, cudaFuncAttributeMaxDynamicSharedMemorySize, kXqBytes);
+    if (first_use_on_device(attr_set)) {
+        cudaFuncSetAttribute(k_tcq_xq<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kXqBytes);
+        cudaFuncSetAttribute(k_tcq_xq<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kXqBytes);
+    }
     const int64_t sms = device_sms();
-    XqArgs a{R, C, row_out, col_sign_bits, col_out, col_prescale, fallbacks, g_tcq_dbg};
+    XqArgs a{R, C, row_out, col_sign_bits, col_out, col_prescale, fallbacks, g_tcq_dbg, 0, 0, 0, R};
+    if (srf_col) {
+        a.srf = 1;
+        a.key = srf_col->sr_base;
+        a.ctr = srf_col->counter_start;
+        a.ld = srf_col->counter_ld ? srf_col->counter_ld : R;
+    }
     const int64_t tiles = ((R + 127) / 128) * ((C + 127) / 128);
-    k_tcq_xq<<<(unsigned)cap_grid(tiles < sms ? tiles : sms), kXqThreads, kXqBytes, st>>>(m, a);
+    const unsigned grid = (unsigned)cap_grid(tiles < sms ? tiles : sms);
+    if (a.srf)
+        k_tcq_xq<true><<<grid, kXqThreads, kXqBytes, st>>>(m, a);
+    else
+        k_tcq_xq<false><<<grid, kXqThreads, kXqBytes, st>>>(m, a);
     return (int)cudaGetLastError();
 }
 

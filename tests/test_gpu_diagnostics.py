@@ -112,3 +112,43 @@ def test_sr_fast_rounds_to_the_same_neighbours():
     assert not torch.equal(a.codes, b.codes)       # a different (hash) stream
     c = quant_rows(x, _lib.QT_TRANSFORM_HADAMARD, _lib.QT_ROUND_SR_FAST, sr_seed=77)
     assert torch.equal(b.codes, c.codes)           # deterministic given the seed
+
+
+@pytest.mark.parametrize("path", ["dual", "fused"])
+def test_tensor_core_sr_fast_matches_cuda_core_sr_fast(path):
+    """QT_ROUND_SR_FAST on the tensor-core quantizers (k_tcq_dual, k_tcq_xq's X_t) draws the same hash uniforms
+    at the same stream positions as the CUDA-core path, for values within the tensor-core error bound of the
+    reference's: the codes agree except where a uniform falls within ~1e-6 of p, and every difference is
+    between the two SR neighbours; the E8M0 scales are identical."""
+    import torch
+
+    from paper_2505_14669_b200 import _lib
+    from paper_2505_14669_b200.mxfp4 import quant_dual, quant_fused, sign_bits
+
+    g = torch.Generator(device="cuda").manual_seed(12)
+    x = (torch.randn(2048, 1024, device="cuda", generator=g) * 3).to(torch.bfloat16)
+    rs, cs = sign_bits(5, 1024, "cuda"), sign_bits(9, 2048, "cuda", start=64)
+    L = _lib.load()
+    outs = []
+    for mode in (0, 1):
+        L.qt_debug_set_quant(mode, None)
+        try:
+            if path == "dual":
+                outs.append(quant_dual(x, _lib.QT_ROUND_SR_FAST, transform=_lib.QT_TRANSFORM_RANDOMIZED, signs=rs,
+                                       col_signs=cs, prescale=0.75, seed_rows=3, seed_cols=4, row_counter_start=99,
+                                       col_counter_start=64, col_counter_ld=4096))
+            else:
+                outs.append(quant_fused(x, _lib.QT_ROUND_QUEST, _lib.QT_ROUND_SR_FAST,
+                                        transform=_lib.QT_TRANSFORM_HADAMARD,
+                                        col_transform=_lib.QT_TRANSFORM_RANDOMIZED, col_signs=cs, col_prescale=0.75,
+                                        col_seed=4, col_counter_start=64, col_counter_ld=4096))
+        finally:
+            L.qt_debug_set_quant(0, None)
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a.scales_rowmajor(), b.scales_rowmajor())
+        ca, cb = a.unpacked_codes(), b.unpacked_codes()
+        diff = ca != cb
+        assert float(diff.float().mean()) < 1e-4, float(diff.float().mean())
+        da, db = a.dequantize(torch.float64), b.dequantize(torch.float64)
+        step = torch.exp2(a.scales_rowmajor().double() - 127).repeat_interleave(32, dim=1) * 2.0
+        assert bool(((da - db).abs() <= step).all())

@@ -46,6 +46,15 @@ for d in (4096, 11008):
                                                     transform=_lib.QT_TRANSFORM_HADAMARD,
                                                     col_transform=_lib.QT_TRANSFORM_RANDOMIZED, col_signs=cs,
                                                     col_prescale=0.75))
+dy = torch.randn(16384, 4096, device="cuda").to(torch.bfloat16)
+rs, cs = sign_bits(5, 4096, "cuda"), sign_bits(9, 16384, "cuda")
+for name, rc in (("sr", _lib.QT_ROUND_SR), ("srfast", _lib.QT_ROUND_SR_FAST)):
+    out[f"dual_{name}_4096"] = timeit(lambda: quant_dual(dy, rc, transform=_lib.QT_TRANSFORM_RANDOMIZED, signs=rs,
+                                                         col_signs=cs, prescale=0.75, seed_rows=1, seed_cols=2))
+    out[f"fusedX_{name}_4096"] = timeit(lambda: quant_fused(dy, _lib.QT_ROUND_QUEST, rc,
+                                                            transform=_lib.QT_TRANSFORM_HADAMARD,
+                                                            col_transform=_lib.QT_TRANSFORM_RANDOMIZED, col_signs=cs,
+                                                            col_prescale=0.75, col_seed=3))
 w = torch.randn(4096, 4096, device="cuda") / 64
 ws = sign_bits(3, 4096, "cuda")
 out["fusedW_4096"] = timeit(lambda: quant_fused(w, _lib.QT_ROUND_QUEST, _lib.QT_ROUND_RTN,
