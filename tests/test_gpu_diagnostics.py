@@ -114,8 +114,9 @@ def test_sr_fast_rounds_to_the_same_neighbours():
     assert torch.equal(b.codes, c.codes)           # deterministic given the seed
 
 
+@pytest.mark.parametrize("grid", [0, 3])
 @pytest.mark.parametrize("path", ["dual", "fused"])
-def test_tensor_core_sr_fast_matches_cuda_core_sr_fast(path):
+def test_tensor_core_sr_fast_matches_cuda_core_sr_fast(path, grid):
     """QT_ROUND_SR_FAST on the tensor-core quantizers (k_tcq_dual, k_tcq_xq's X_t) draws the same hash uniforms
     at the same stream positions as the CUDA-core path, for values within the tensor-core error bound of the
     reference's: the codes agree except where a uniform falls within ~1e-6 of p, and every difference is
@@ -130,20 +131,24 @@ def test_tensor_core_sr_fast_matches_cuda_core_sr_fast(path):
     rs, cs = sign_bits(5, 1024, "cuda"), sign_bits(9, 2048, "cuda", start=64)
     L = _lib.load()
     outs = []
-    for mode in (0, 1):
-        L.qt_debug_set_quant(mode, None)
-        try:
-            if path == "dual":
-                outs.append(quant_dual(x, _lib.QT_ROUND_SR_FAST, transform=_lib.QT_TRANSFORM_RANDOMIZED, signs=rs,
-                                       col_signs=cs, prescale=0.75, seed_rows=3, seed_cols=4, row_counter_start=99,
-                                       col_counter_start=64, col_counter_ld=4096))
-            else:
-                outs.append(quant_fused(x, _lib.QT_ROUND_QUEST, _lib.QT_ROUND_SR_FAST,
-                                        transform=_lib.QT_TRANSFORM_HADAMARD,
-                                        col_transform=_lib.QT_TRANSFORM_RANDOMIZED, col_signs=cs, col_prescale=0.75,
-                                        col_seed=4, col_counter_start=64, col_counter_ld=4096))
-        finally:
-            L.qt_debug_set_quant(0, None)
+    L.qt_debug_set_grid(grid)       # 3 CTAs: every CTA walks many tiles (stage / TMEM reuse)
+    try:
+        for mode in (0, 1):
+            L.qt_debug_set_quant(mode, None)
+            try:
+                if path == "dual":
+                    outs.append(quant_dual(x, _lib.QT_ROUND_SR_FAST, transform=_lib.QT_TRANSFORM_RANDOMIZED, signs=rs,
+                                           col_signs=cs, prescale=0.75, seed_rows=3, seed_cols=4, row_counter_start=99,
+                                           col_counter_start=64, col_counter_ld=4096))
+                else:
+                    outs.append(quant_fused(x, _lib.QT_ROUND_QUEST, _lib.QT_ROUND_SR_FAST,
+                                            transform=_lib.QT_TRANSFORM_HADAMARD,
+                                            col_transform=_lib.QT_TRANSFORM_RANDOMIZED, col_signs=cs, col_prescale=0.75,
+                                            col_seed=4, col_counter_start=64, col_counter_ld=4096))
+            finally:
+                L.qt_debug_set_quant(0, None)
+    finally:
+        L.qt_debug_set_grid(0)
     for a, b in zip(outs[0], outs[1]):
         assert torch.equal(a.scales_rowmajor(), b.scales_rowmajor())
         ca, cb = a.unpacked_codes(), b.unpacked_codes()
