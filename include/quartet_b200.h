@@ -247,7 +247,7 @@ QT_API int qt_seam_row_sums(const double* a, const double* b, int op, int64_t ro
  *   strides stride_b / stride_s / stride_h, head_dim contiguous) with cos/sin tables [seq, head_dim], into a
  *   contiguous out; backward != 0 applies the transposed rotation (dx from dy).
  * qt_swiglu: forward out0 = silu(gate) * up; backward (dy given) out0 = d gate, out1 = d up.  n % 8 == 0.
- * qt_rmsnorm: rows of x [rows, d] bf16 (d % 256 == 0 up to 2048, or d in {4096, 6144, 8192}), fp32 weight w: forward out = x rstd w and
+ * qt_rmsnorm: rows of x [rows, d] bf16 (d % 8 == 0 up to 2048, or d in {4096, 6144, 8192}), fp32 weight w: forward out = x rstd w and
  *   rstd[rows] saved; backward (dy, rstd given) out = dx, dw[d] += sum over rows (caller zeroes dw).
  * qt_cross_entropy: rows of logits [rows, vocab] bf16 (vocab % 8 == 0), int64 targets: forward writes lse and
  *   the per-row loss (fp32); backward writes dlogits = (softmax - onehot) * (*dloss) * scale (bf16). */

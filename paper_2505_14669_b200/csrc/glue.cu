@@ -105,22 +105,22 @@ __global__ void k_swiglu(const uint4* __restrict__ g, const uint4* __restrict__ 
     }
 }
 
-// RMSNorm over rows of x [rows, d] bf16 with an fp32 weight, one warp per row (d % 256 == 0, d <= 2048):
+// RMSNorm over rows of x [rows, d] bf16 with an fp32 weight, one warp per row (d % 8 == 0, d <= 2048):
 // forward y = x * rstd * w (rstd = 1/sqrt(mean(x^2) + eps) in fp32, saved); backward dx = rstd (g - xh mean(g xh))
 // with g = dy * w, xh = x * rstd, and dw += sum_rows dy * xh (per-warp partials -> smem -> one atomic per
-// column per block).
-template <int NV>  // uint4 chunks of 8 bf16 per lane: d = 256 * NV
+// column per block).  Lane `lane` owns the 16-byte chunks v * 32 + lane (v < NV) that lie inside the row.
+template <int NV>  // uint4 chunks of 8 bf16 per lane: d <= 256 * NV
 __global__ void k_rmsnorm(const uint4* __restrict__ x, const float* __restrict__ w, const uint4* __restrict__ dy,
                           uint4* __restrict__ out, float* __restrict__ rstd_io, float* __restrict__ dw, int64_t rows,
-                          float eps, int backward) {
-    constexpr int D = 256 * NV;
-    extern __shared__ float red[];  // [warps][D] partial dw (backward)
+                          int d, float eps, int backward) {
+    extern __shared__ float red[];  // [warps][d] partial dw (backward)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int nch = d / 8;          // chunks per row
     float wv[NV][8];
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
-        for (int t = 0; t < 8; ++t) wv[v][t] = w[(v * 32 + lane) * 8 + t];
+        for (int t = 0; t < 8; ++t) wv[v][t] = v * 32 + lane < nch ? w[(v * 32 + lane) * 8 + t] : 0.f;
     float dwp[NV][8];
 #pragma unroll
     for (int v = 0; v < NV; ++v)
@@ -131,7 +131,8 @@ __global__ void k_rmsnorm(const uint4* __restrict__ x, const float* __restrict__
         float ss = 0.f;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-            const uint4 c = x[r * (D / 8) + v * 32 + lane];
+            const bool ok = v * 32 + lane < nch;
+            const uint4 c = ok ? x[r * nch + v * 32 + lane] : make_uint4(0, 0, 0, 0);
             const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
@@ -142,54 +143,59 @@ __global__ void k_rmsnorm(const uint4* __restrict__ x, const float* __restrict__
         if (!backward) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-            const float rs = rsqrtf(ss / (float)D + eps);
+            const float rs = rsqrtf(ss / (float)d + eps);
             if (lane == 0) rstd_io[r] = rs;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
+                if (v * 32 + lane >= nch) continue;
                 uint32_t o4[4];
 #pragma unroll
                 for (int t = 0; t < 4; ++t)
                     o4[t] = pack_bf2(xv[v][2 * t] * rs * wv[v][2 * t], xv[v][2 * t + 1] * rs * wv[v][2 * t + 1]);
-                out[r * (D / 8) + v * 32 + lane] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+                out[r * nch + v * 32 + lane] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
             }
         } else {
             const float rs = rstd_io[r];
             float gv[NV][8], dot = 0.f;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-                const uint4 c = dy[r * (D / 8) + v * 32 + lane];
+                const bool ok = v * 32 + lane < nch;
+                const uint4 c = ok ? dy[r * nch + v * 32 + lane] : make_uint4(0, 0, 0, 0);
                 const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
-                    const float d = bf(cw[t >> 1], t & 1), xh = xv[v][t] * rs;
-                    gv[v][t] = d * wv[v][t];
+                    const float dd = bf(cw[t >> 1], t & 1), xh = xv[v][t] * rs;
+                    gv[v][t] = dd * wv[v][t];
                     dot = fmaf(gv[v][t], xh, dot);
-                    dwp[v][t] = fmaf(d, xh, dwp[v][t]);
+                    dwp[v][t] = fmaf(dd, xh, dwp[v][t]);
                 }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-            const float mdot = dot / (float)D;
+            const float mdot = dot / (float)d;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
+                if (v * 32 + lane >= nch) continue;
                 uint32_t o4[4];
 #pragma unroll
                 for (int t = 0; t < 4; ++t)
                     o4[t] = pack_bf2(rs * (gv[v][2 * t] - xv[v][2 * t] * rs * mdot),
                                      rs * (gv[v][2 * t + 1] - xv[v][2 * t + 1] * rs * mdot));
-                out[r * (D / 8) + v * 32 + lane] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+                out[r * nch + v * 32 + lane] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
             }
         }
     }
     if (backward) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v)
+        for (int v = 0; v < NV; ++v) {
+            if (v * 32 + lane >= nch) continue;
 #pragma unroll
-            for (int t = 0; t < 8; ++t) red[wib * D + (v * 32 + lane) * 8 + t] = dwp[v][t];
+            for (int t = 0; t < 8; ++t) red[wib * d + (v * 32 + lane) * 8 + t] = dwp[v][t];
+        }
         __syncthreads();
-        for (int c = threadIdx.x; c < D; c += blockDim.x) {
+        for (int c = threadIdx.x; c < d; c += blockDim.x) {
             float sum = 0.f;
-            for (int k = 0; k < nw; ++k) sum += red[k * D + c];
+            for (int k = 0; k < nw; ++k) sum += red[k * d + c];
             atomicAdd(dw + c, sum);
         }
     }
@@ -386,7 +392,7 @@ QT_API int qt_rope(const void* x, void* out, int64_t rows, int heads, int head_d
 
 QT_API int qt_rmsnorm(const void* x, const float* w, const void* dy, void* out, float* rstd, float* dw, int64_t rows,
                       int d, float eps, int backward, void* stream) {
-    if (rows < 0 || d % 256 != 0 || d < 256 || (d > 2048 && (d % 2048 != 0 || d > 8192))) return QT_ERR_SHAPE;
+    if (rows < 0 || d % 8 != 0 || d < 8 || (d > 2048 && (d % 2048 != 0 || d > 8192))) return QT_ERR_SHAPE;
     if (!al16(x) || !al16(out) || (backward && (!al16(dy) || !dw))) return QT_ERR_ALIGN;
     if (rows == 0) return 0;
     if (d > 2048) {
@@ -411,9 +417,9 @@ QT_API int qt_rmsnorm(const void* x, const float* w, const void* dy, void* out, 
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<blocks, warps * 32, smem, (cudaStream_t)stream>>>(static_cast<const uint4*>(x), w,
                                                                static_cast<const uint4*>(dy), static_cast<uint4*>(out),
-                                                               rstd, dw, rows, eps, backward);
+                                                               rstd, dw, rows, d, eps, backward);
     };
-    switch (d / 256) {
+    switch ((d + 255) / 256) {
         case 1: go(k_rmsnorm<1>); break;
         case 2: go(k_rmsnorm<2>); break;
         case 3: go(k_rmsnorm<3>); break;

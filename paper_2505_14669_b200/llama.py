@@ -74,7 +74,7 @@ class RMSNorm(torch.nn.Module):
 
     def forward(self, x):  # bf16 in / out, fp32 statistics and weight
         d = x.shape[-1]
-        if d % 256 == 0 and (d <= 2048 or (d % 2048 == 0 and d <= 8192)):  # csrc/glue.cu, one pass each way
+        if d % 8 == 0 and (d <= 2048 or (d % 2048 == 0 and d <= 8192)):  # csrc/glue.cu, one pass each way
             return _RMSNormFn.apply(x.to(torch.bfloat16), self.weight, self.eps)
         return F.rms_norm(x.to(torch.bfloat16), (d,), self.weight.to(torch.bfloat16), self.eps)
 

@@ -68,7 +68,7 @@ def test_glue_entry_points_reject_bad_shapes(lib):
     assert lib.qt_rope(None, None, 64, 2, 10, 64, None, None, 0, 0, 0, 0, None) == 2001      # head_dim % 16
     assert lib.qt_rope(None, None, 65, 2, 16, 64, None, None, 0, 0, 0, 0, None) == 2001      # rows % seq
     assert lib.qt_swiglu(None, None, None, None, None, 7, 0, None) == 2001                   # n % 8
-    assert lib.qt_rmsnorm(None, None, None, None, None, None, 8, 100, 1e-6, 0, None) == 2001  # d % 256
+    assert lib.qt_rmsnorm(None, None, None, None, None, None, 8, 100, 1e-6, 0, None) == 2001  # d % 8
     assert lib.qt_rmsnorm(None, None, None, None, None, None, 8, 10240, 1e-6, 0, None) == 2001
     assert lib.qt_cross_entropy(None, None, 8, 7, None, None, None, None, 1.0, 0, None) == 2001
 

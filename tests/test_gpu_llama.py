@@ -91,7 +91,7 @@ def test_fused_swiglu_matches_fp32_reference(llama):
     torch.testing.assert_close(du.float(), duf, rtol=2 ** -7, atol=1e-4)
 
 
-@pytest.mark.parametrize("d", [1280, 4096])
+@pytest.mark.parametrize("d", [640, 1280, 1800, 4096])
 def test_fused_rmsnorm_matches_fp32_reference(llama, d):
     """csrc/glue.cu RMSNorm (forward, dx, dw; warp-per-row and block-per-row variants) vs an fp32 torch
     reference; tolerance: bf16 rounding of the outputs (2^-7 relative) and fp32 summation order for dw."""
