@@ -676,7 +676,16 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     if out is not None:
-        print(json.dumps(out), flush=True)
+        # contract keys first, the long per-kernel table and the train section last (a truncated log tail still
+        # shows the headline fields)
+        head = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "e2e", "roofline", "cpu_baseline", "bf16_cublas",
+                "quantizer_roofline", "gpu_launches", "clocks", "tokens_per_s", "sr_backward", "sr_fast_backward")
+        tail = ("train", "kernels")
+        ordered = {k: out[k] for k in head if k in out}
+        ordered.update({k: v for k, v in out.items() if k not in head and k not in tail})
+        ordered.update({k: out[k] for k in tail if k in out})
+        print(json.dumps(ordered), flush=True)
 
 
 if __name__ == "__main__":
