@@ -1,8 +1,8 @@
-"""Epilogue staging variants of the 2-CTA GEMM on the bench's nine GEMMs (16384 tokens, Llama-7B shapes):
-time per variant (variants interleaved, 3 rounds, best) and bit-equality with the production path.
+"""2-CTA GEMM epilogue experiments (timing only): cost of the output stores and of the epilogue math.
 
-    python tools/gemm_epi_probe.py [dbg ...]      (timing knobs: 0x100 no epilogue, 0x200 no TMA stores, 0x400 no mask/FWHT/scale)
-"""
+profiles/r02_gemm_epilogue_probe.txt also holds a "direct st.global" arm (a dbg knob, since removed, that
+stored the accumulator rows from registers with epi_store instead of the staged TMA stores): 4-35 % slower
+than the staged stores at every shape, so the staged path stays."""
 import ctypes
 import os
 import sys
@@ -15,50 +15,48 @@ from paper_2505_14669_b200 import _lib  # noqa: E402
 
 L = qt.load()
 L.qt_debug_set_gemm.argtypes = [ctypes.c_int]
-T = 16384
-VARIANTS = [0] + [int(a, 0) for a in sys.argv[1:]] if len(sys.argv) > 1 else [0, 0x100, 0x200, 0x400]
+dev = "cuda"
 
 
-def timed(fn, reps=10):
-    for _ in range(2):
-        fn()
+def t(f):
+    for _ in range(3):
+        f()
     torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for _ in range(reps):
-        fn()
-    e.record()
-    torch.cuda.synchronize()
-    return s.elapsed_time(e) * 1e3 / reps
+    best = []
+    for _ in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(10):
+            f()
+        e.record()
+        torch.cuda.synchronize()
+        best.append(s.elapsed_time(e) * 100)
+    return sorted(best)[1]
 
 
-def operand(r, c):
-    return qt.quant_rows(torch.randn(r, c, device="cuda").to(torch.bfloat16), 0, _lib.QT_ROUND_RTN)
-
-
-totals = {v: 0.0 for v in VARIANTS}
-for d_in, d_out in [(4096, 4096), (4096, 11008), (11008, 4096)]:
-    cases = [("fwd", operand(T, d_in), operand(d_out, d_in), torch.bfloat16, None),
-             ("dx", operand(T, d_out), operand(d_in, d_out), torch.bfloat16,
-              torch.randint(-2**31, 2**31 - 1, (T, d_in // 32), device="cuda", dtype=torch.int32)),
-             ("dw", operand(d_out, T), operand(d_in, T), torch.float32,
-              torch.randint(-2**31, 2**31 - 1, (d_out, d_in // 32), device="cuda", dtype=torch.int32))]
-    for name, A, B, odt, mask in cases:
-        kw = {} if mask is None else {"mask": mask, "hadamard": True, "scale": 16 / 9}
-        out = torch.empty(A.rows, B.rows, device="cuda", dtype=odt)
-        L.qt_debug_set_gemm(0)
-        ref = qt.gemm(A, B, out_dtype=odt, **kw)
-        best = {v: 1e30 for v in VARIANTS}
-        same = {v: True for v in VARIANTS}
-        for _ in range(3):
-            for v in VARIANTS:
-                L.qt_debug_set_gemm(v)
-                best[v] = min(best[v], timed(lambda: qt.gemm(A, B, out=out, **kw)))
-                same[v] &= torch.equal(out, ref)
-        L.qt_debug_set_gemm(0)
-        for v in VARIANTS:
-            totals[v] += best[v]
-        print(f"{d_in}->{d_out} {name:3s} M{A.rows} N{B.rows} K{A.cols}: " +
-              " | ".join(f"{v:#x} {best[v]:7.1f}{'' if same[v] else ' MISMATCH'}" for v in VARIANTS), flush=True)
-        del out, ref
-print("sum over the 9 GEMMs (us): " + " | ".join(f"{v:#x} {t:.1f}" for v, t in totals.items()))
+for (M, N, K) in [(16384, 4096, 4096), (16384, 11008, 4096), (16384, 4096, 11008), (4096, 4096, 16384)]:
+    x = torch.randn(M, K, device=dev).to(torch.bfloat16)
+    w = torch.randn(N, K, device=dev).to(torch.bfloat16)
+    A = qt.quant_rows(x, 0, _lib.QT_ROUND_RTN)
+    B = qt.quant_rows(w, 0, _lib.QT_ROUND_RTN)
+    mask = torch.randint(0, 2**31 - 1, (M, N // 32), device=dev, dtype=torch.int32)
+    for odt in (torch.bfloat16, torch.float32):
+        out = torch.empty(M, N, device=dev, dtype=odt)
+        for epi in ("store", "maskH"):
+            kw = dict(mask=mask, hadamard=True, scale=16 / 9) if epi == "maskH" else {}
+            ref = None
+            for dbg, name in [(0, "staged TMA"), (0x200, "no TMA stores"),
+                              (0x400, "no math"), (0x100, "no epilogue")]:
+                L.qt_debug_set_gemm(dbg)
+                us = t(lambda: qt.gemm(A, B, out=out, **kw))
+                if dbg == 0:
+                    o = out.clone()
+                    if ref is None:
+                        ref = o
+                    same = bool(torch.equal(ref, o))
+                else:
+                    same = ""
+                print(f"M{M} N{N} K{K} {str(odt)[6:]:8s} {epi:5s} {name:18s} {us:8.1f} us "
+                      f"{2 * M * N * K / us / 1e6:7.1f} TF {same}", flush=True)
+            L.qt_debug_set_gemm(0)
+        del out
