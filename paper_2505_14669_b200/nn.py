@@ -85,7 +85,8 @@ class QuartetLinearFn(torch.autograd.Function):
 
 class QuartetLinearGroupFn(torch.autograd.Function):
     """Several Quartet linears reading the same x (q/k/v, gate/up): X_q and M_x = QuEST(H32 x) are computed
-    once (they depend on x alone), each layer derives its own X_t (its own xi) from X_q's codes, and the
+    once (they depend on x alone; the first layer's fused quantizer pass also gives its own X_t), the other
+    layers derive their X_t (their own xi) from X_q's codes, and the
     input gradients of the layers are summed in x's dtype (as autograd accumulates separate layers' dx).
     Outputs and weight gradients are bit-identical to separate QuartetLinearFn calls."""
 
@@ -96,13 +97,15 @@ class QuartetLinearGroupFn(torch.autograd.Function):
         if x2.dtype not in (torch.bfloat16, torch.float32):
             x2 = x2.float()
         ctx.shard = shard
-        x_q = qlinear.quantize_operand(x2, scheme, hadamard, err=nonfinite_flag(x.device))
         out_dtype = x.dtype if x.dtype in (torch.bfloat16, torch.float32) else torch.float32
         ys, ctx.lctxs = [], []
+        # the first layer quantizes x in one fused pass (X_q, M_x and its own X_t); the others reuse its X_q
+        x_q = None
         for w, xi, xd in zip(ws, xis, xi_devs):
             y, lctx = qlinear.forward(x2, w.detach(), scheme=scheme, hadamard=hadamard, out_dtype=out_dtype,
                                       check_finite=nonfinite_flag(x.device), bwd_xi=int(xi), bwd_rounding=rounding,
                                       token_offset=shard[0], total_tokens=shard[1], x_q=x_q, bwd_xi_dev=xd)
+            x_q = lctx.x_q
             ys.append(y.reshape(*lead, w.shape[0]))
             ctx.lctxs.append(lctx)
         ctx.xis, ctx.rounding, ctx.x_shape, ctx.x_dtype = [int(v) for v in xis], rounding, x.shape, x.dtype

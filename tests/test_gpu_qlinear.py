@@ -172,7 +172,7 @@ def test_autograd_function_and_module(qt):
     assert torch.equal(y2, y_ref)
 
 
-@pytest.mark.parametrize("rounding", ["rtn", "sr"])
+@pytest.mark.parametrize("rounding", ["rtn", "sr", "sr_fast"])
 def test_group_of_linears_sharing_x_matches_separate_layers(rounding):
     """quartet_linear_group (one QuEST read of x for q/k/v-style layers) gives bit-identical outputs and
     weight gradients to separate QuartetLinear calls; dx agrees to bf16 rounding of the summed gradient."""
