@@ -57,13 +57,36 @@ class MXOperand:
         mask = torch.empty((rows, cols // GROUP), dtype=torch.int32, device=device) if with_mask else None
         return MXOperand(codes, sf, rows, cols, mask)
 
+    def pad_rows(self, rows: int) -> "MXOperand":
+        """This operand with zero rows appended up to `rows` (codes 0, E8M0 byte 0, mask 0): the operand of
+        the zero-padded matrix.  Used where the reference quantizes a ragged trailing group along this
+        operand's rows (qlinear.backward with hadamard=False)."""
+        if rows < self.rows:
+            raise ValueError(f"pad_rows: {rows} < {self.rows}")
+        if rows == self.rows:
+            return self
+        dev = self.codes.device
+        codes = torch.zeros((rows, self.cols // 2), dtype=torch.uint8, device=dev)
+        codes[:self.rows] = self.codes
+        sf = torch.zeros(int(_lib.load().qt_sf_bytes(rows, self.cols)), dtype=torch.uint8, device=dev)
+        off = self._sf_offsets()
+        sf[off] = self.sf[off]
+        mask = None
+        if self.mask is not None:
+            mask = torch.zeros((rows, self.cols // GROUP), dtype=torch.int32, device=dev)
+            mask[:self.rows] = self.mask
+        return MXOperand(codes, sf, rows, self.cols, mask)
+
     # ---------------------------------------------------------------- parity helpers
-    def scales_rowmajor(self) -> torch.Tensor:
-        """uint8 [rows, cols/32] in the reference layout (QuantizedTensor.scales)."""
+    def _sf_offsets(self) -> torch.Tensor:
+        """[rows, cols/32] byte offsets of the E8M0 scales in the scale-atom buffer."""
         r = torch.arange(self.rows, device=self.sf.device).view(-1, 1)
         g = torch.arange(self.cols // GROUP, device=self.sf.device).view(1, -1)
-        off = ((r >> 7) * self.katoms + (g >> 2)) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (g & 3)
-        return self.sf[off]
+        return ((r >> 7) * self.katoms + (g >> 2)) * 512 + (r & 31) * 16 + ((r >> 5) & 3) * 4 + (g & 3)
+
+    def scales_rowmajor(self) -> torch.Tensor:
+        """uint8 [rows, cols/32] in the reference layout (QuantizedTensor.scales)."""
+        return self.sf[self._sf_offsets()]
 
     def mask_bool(self) -> torch.Tensor:
         """bool [rows, cols]: the reference's m_x / m_w."""

@@ -248,11 +248,52 @@ def forward(x: torch.Tensor, w: torch.Tensor, scheme: QuantScheme = QUEST, polic
         if x_q is None:
             x_q = quantize_operand(x, scheme, hadamard, sx, err, row_offset=token_offset)
         w_q = quantize_operand(w, scheme, hadamard, sw, err)
-    y = gemm(x_q, w_q, out_dtype=out_dtype)
+    if d_out % g:   # ragged d_out (the GEMM's N axis is whole blocks): zero rows of W_q, sliced off y
+        y = gemm(x_q, w_q.pad_rows(-(-d_out // g) * g), out_dtype=out_dtype)[:, :d_out].contiguous()
+    else:
+        y = gemm(x_q, w_q, out_dtype=out_dtype)
     _raise_if_nonfinite(err, check_finite)
     ctx = LayerContext(x_q=x_q, w_q=w_q, scheme=scheme, policy=policy, hadamard=hadamard,
                        batch=batch, d_in=d_in, d_out=d_out, eager=eager)
     return y, ctx
+
+
+def _backward_ragged(dy, ctx, xi, rounding, rc, dx_dtype, dw_dtype, check_finite, return_operands, token_offset,
+                     total, dx_accumulate):
+    """backward with hadamard=False and d_out or batch not a multiple of 32: the reference quantizes a
+    ragged trailing group of G (along d_out), W_t (along d_out), G_t and X_t (along tokens) (qlinear.py:
+    212-250, codec ragged groups).  Every operand is built from the zero-padded matrix: a zero pads a group
+    without changing its absmax scale, encodes as code 0 under RTN and SR alike (p = 0), and adds nothing
+    to the dx / dw contractions; the SR stream positions are those of the unpadded matrices (counter
+    leading dimensions d_out and the token count).  Operands are returned padded (return_operands)."""
+    g = ctx.scheme.group_size
+    B, D = ctx.batch, ctx.d_out
+    Bp, Dp = -(-B // g) * g, -(-D // g) * g
+    sr = rounding in ("sr", "sr_fast")
+    none = _lib.QT_TRANSFORM_NONE
+    err = _err_for(check_finite, dy.device)
+    dy_p = torch.zeros((Bp, Dp), dtype=dy.dtype if dy.dtype in (torch.bfloat16, torch.float32) else torch.float32,
+                       device=dy.device)
+    dy_p[:B, :D] = dy
+    x_q, w_q = ctx.x_q.pad_rows(Bp), ctx.w_q.pad_rows(Dp)
+    g_q = quant_rows(dy_p, none, rc, prescale=PRE_SCALE, sr_seed=derive_seed(xi, _TAG_BWD_G1) if sr else 0,
+                     counter_start=token_offset * D, counter_ld=D, err=err)
+    wt_q = quant_cols(w_q, rc, transform=none, prescale=PRE_SCALE, sr_seed=derive_seed(xi, _TAG_BWD_W) if sr else 0,
+                      counter_ld=D, err=err)
+    dx_dt = dx_accumulate.dtype if dx_accumulate is not None else dx_dtype
+    dx = gemm(g_q, wt_q, out_dtype=dx_dt, mask=x_q.mask, hadamard=False, scale=_POST_F32)[:B]
+    if dx_accumulate is not None:
+        dx = dx_accumulate.add_(dx)
+    gt_q = quant_cols(dy_p, rc, transform=none, prescale=PRE_SCALE,
+                      sr_seed=derive_seed(xi, _TAG_BWD_G2) if sr else 0, counter_start=token_offset,
+                      counter_ld=total, err=err)
+    xt_q = quant_cols(x_q, rc, transform=none, prescale=PRE_SCALE, sr_seed=derive_seed(xi, _TAG_BWD_X) if sr else 0,
+                      counter_start=token_offset, counter_ld=total, err=err)
+    dw = gemm(gt_q, xt_q, out_dtype=dw_dtype, mask=w_q.mask, hadamard=False, scale=_POST_F32)[:D]
+    _raise_if_nonfinite(err, check_finite)
+    if return_operands:
+        return dx, dw, {"g_q": g_q, "wt_q": wt_q, "gt_q": gt_q, "xt_q": xt_q}
+    return dx, dw
 
 
 def _check_out_dtype(name: str, dt: torch.dtype) -> None:
@@ -290,10 +331,9 @@ def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn"
     and the sum of the ranks' dw equals the single-GPU dw up to fp32 summation order (the masked
     Hadamard epilogue is linear).  token_offset must be a multiple of 32.
 
-    Restriction vs the reference: d_out and batch must be multiples of the block size even with
-    hadamard=False (the reference checks them only for hadamard=True and quantizes a ragged trailing
-    group).  They are the contraction axes of the dx / dw GEMMs, whose MXFP4 operands are whole
-    32-element blocks; ragged shapes raise ValueError here (INTEGRATION.md lists the rejected cases)."""
+    d_out and batch must be multiples of the block size with hadamard=True (ValueError, as the reference);
+    with hadamard=False the reference quantizes a ragged trailing group, and so does this path
+    (_backward_ragged)."""
     if rounding not in ("exact", "rtn", "sr", "sr_fast"):
         raise ValueError(f"unknown backward rounding {rounding!r}")
     rc = _rounding_code(rounding)
@@ -303,13 +343,16 @@ def backward(dy: torch.Tensor, ctx: LayerContext, xi: int, rounding: str = "rtn"
     if tuple(dy.shape) != (ctx.batch, ctx.d_out):
         raise ValueError(f"dy shape {tuple(dy.shape)}, expected {(ctx.batch, ctx.d_out)}")
     g = ctx.scheme.group_size
-    if ctx.d_out % g != 0:
+    if ctx.hadamard and ctx.d_out % g != 0:
         raise ValueError(f"output dimension {ctx.d_out} not divisible by block size {g}")
-    if ctx.batch % g != 0:
+    if ctx.hadamard and ctx.batch % g != 0:
         raise ValueError(f"batch size {ctx.batch} not divisible by block size {g}")
     total = ctx.batch if total_tokens is None else int(total_tokens)
     if token_offset % g or token_offset < 0 or token_offset + ctx.batch > total:
         raise ValueError(f"token shard [{token_offset}, +{ctx.batch}) invalid for {total} tokens (block {g})")
+    if ctx.d_out % g or ctx.batch % g:
+        return _backward_ragged(dy, ctx, xi, rounding, rc, dx_dtype, dw_dtype, check_finite, return_operands,
+                                token_offset, total, dx_accumulate)
     dev = dy.device
     transform = _lib.QT_TRANSFORM_RANDOMIZED if ctx.hadamard else _lib.QT_TRANSFORM_NONE
     ea = ctx.eager

@@ -157,6 +157,10 @@ def main():
         ("quest_rtn_noh", 64, 64, 96, QUEST, False, "rtn", 5),
         ("srfwd_sr", 64, 128, 96, SR_ABSMAX, True, "sr", 13, 99),
         ("srfwd_rtn_t256", 256, 96, 128, SR_ABSMAX, True, "rtn", 17, 2**64 - 3),
+        # hadamard=False accepts ragged batch / d_out: ragged trailing groups in G, W_t, G_t, X_t
+        ("quest_rtn_noh_ragged", 201, 64, 77, QUEST, False, "rtn", 5),
+        ("quest_sr_noh_ragged", 72, 96, 40, QUEST, False, "sr", 9),
+        ("rtnfwd_sr_noh_ragged", 45, 64, 33, RTN_ABSMAX, False, "sr", 21),
     ]
     for name, T, d_in, d_out, scheme, had, rounding, xi, *fseed in cases:
         if os.environ.get("GOLDEN_ONLY") and name not in os.environ["GOLDEN_ONLY"].split(","):

@@ -16,7 +16,8 @@ from gpu_util import assert_operand_equal, bf16_values, rel_err, to_dev
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 TOL = 1e-5
-GOLDEN_CASES = ["quest_rtn", "quest_sr", "quest_rtn_t256", "rtnfwd_rtn", "quest_rtn_noh", "srfwd_sr", "srfwd_rtn_t256"]
+GOLDEN_CASES = ["quest_rtn", "quest_sr", "quest_rtn_t256", "rtnfwd_rtn", "quest_rtn_noh", "srfwd_sr", "srfwd_rtn_t256",
+                "quest_rtn_noh_ragged", "quest_sr_noh_ragged", "rtnfwd_sr_noh_ragged"]
 
 
 @pytest.fixture(scope="module")
@@ -43,7 +44,8 @@ def test_golden_end_to_end(qt, oracle, case, eager):
     kw = dict(bwd_xi=int(z["xi"]), bwd_rounding=str(z["rounding"])) if eager else {}
     y, ctx = qt.forward(to_dev(z["x"], torch.bfloat16), to_dev(z["w"], torch.bfloat16),
                         scheme=_scheme(qt, str(z["scheme"])), hadamard=had, seed=seed, **kw)
-    assert (ctx.eager is not None) == eager
+    whole = z["x"].shape[0] % 32 == 0 and z["w"].shape[0] % 32 == 0   # ragged shapes take the lazy path
+    assert (ctx.eager is not None) == (eager and whole)
     # saved context: bit-exact against the reference's LayerContext
     assert np.array_equal(ctx.x_q.codes.cpu().numpy(), z["x_codes"])
     assert np.array_equal(ctx.x_q.scales_rowmajor().cpu().numpy(), z["x_scales"])
@@ -62,6 +64,27 @@ def test_golden_end_to_end(qt, oracle, case, eager):
     for name, key in (("g_q", "gq"), ("wt_q", "wtq"), ("gt_q", "gtq"), ("xt_q", "xtq")):
         c, s = octx.inter[key]
         assert_operand_equal(ops[name], c, s, name)
+
+
+@pytest.mark.parametrize("shape", [(50, 64, 45), (96, 128, 200), (33, 32, 1)])
+def test_ragged_forward_with_hadamard(qt, oracle, shape):
+    """The reference's forward takes any batch and d_out (only d_in must be whole blocks, qlinear.py:114-165);
+    backward then needs whole blocks of d_out and batch when hadamard=True and raises ValueError otherwise."""
+    T, d_in, d_out = shape
+    r = np.random.default_rng(T * 1000 + d_out)
+    x = bf16_values(r.normal(size=(T, d_in)).astype(np.float32))
+    w = bf16_values((r.normal(size=(d_out, d_in)) / np.sqrt(d_in)).astype(np.float32))
+    y_ref, octx = oracle.forward(x, w)
+    y, ctx = qt.forward(to_dev(x, torch.bfloat16), to_dev(w, torch.bfloat16), bwd_xi=3)
+    assert ctx.eager is None
+    assert_operand_equal(ctx.x_q, octx.x_codes, octx.x_scales, "X_q")
+    assert_operand_equal(ctx.w_q, octx.w_codes, octx.w_scales, "W_q")
+    assert tuple(y.shape) == (T, d_out)
+    assert rel_err(y.cpu().numpy(), y_ref) <= TOL
+    dy = torch.randn(T, d_out, device="cuda", dtype=torch.bfloat16)
+    if T % 32 or d_out % 32:
+        with pytest.raises(ValueError, match="not divisible"):
+            qt.backward(dy, ctx, xi=3)
 
 
 @pytest.mark.parametrize("eager", [False, True], ids=["lazy", "eager"])

@@ -73,7 +73,8 @@ def test_threads_do_not_change_results(oracle, golden_dir):
         assert np.array_equal(a, b)
 
 
-CASES = ["quest_rtn", "quest_sr", "quest_rtn_t256", "rtnfwd_rtn", "quest_rtn_noh", "srfwd_sr", "srfwd_rtn_t256"]
+CASES = ["quest_rtn", "quest_sr", "quest_rtn_t256", "rtnfwd_rtn", "quest_rtn_noh", "srfwd_sr", "srfwd_rtn_t256",
+         "quest_rtn_noh_ragged", "quest_sr_noh_ragged", "rtnfwd_sr_noh_ragged"]
 
 
 @pytest.mark.parametrize("case", CASES)
