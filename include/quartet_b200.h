@@ -68,10 +68,12 @@ extern "C" {
 #define QT_ROUND_QUEST 0           /* quantize_quest, ratio_lo = 1/16 (_native.pyx:206-245) */
 #define QT_ROUND_RTN 1             /* quantize_rtn (_native.pyx:104-131) */
 #define QT_ROUND_SR 2              /* quantize_sr (_native.pyx:134-168) */
-#define QT_ROUND_SR_FAST 3         /* B200 extension: stochastic rounding with the same neighbours and p as QT_ROUND_SR,
-                                      against 24-bit uniforms from a 32-bit hash of (seed, stream position) --
-                                      statistically unbiased, not the reference's splitmix64 draws (quantizer entry
-                                      points only; the seam and the diagnostics keep the reference's streams) */
+#define QT_ROUND_SR_FAST 3         /* B200 extension: stochastic rounding to the same two neighbours as QT_ROUND_SR by
+                                      the hardware conversion cvt.rs.satfinite.e2m1x4.f32 (32 hashed random bits of
+                                      (seed, stream position) per 4 elements): P(upper) = floor(p * 2^16) / 2^16,
+                                      unbiased up to 2^-16 of a grid step, not the reference's splitmix64 draws
+                                      (quantizer entry points only; the seam and the diagnostics keep the
+                                      reference's streams) */
 #define QT_EPI_STORE 0             /* D = A B^T */
 #define QT_EPI_MASK_H 1            /* D = H32(A B^T (.) mask) * scale (qlinear.py:229-230, 249-250) */
 #define QT_EPI_MASK 2              /* D = (A B^T (.) mask) * scale (hadamard=False layers) */

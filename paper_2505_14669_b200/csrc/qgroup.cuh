@@ -288,16 +288,14 @@ __device__ __forceinline__ int quant_group(float (&v)[32], const QuantCfg& cf, u
         const double sc_d = (double)sc_f;
         uint32_t w[4];
         if (cf.sr_fast) {   // QT_ROUND_SR_FAST: statistically unbiased, not the reference's stream
-            const uint32_t k0 = (uint32_t)cf.sr_base, k1 = (uint32_t)(cf.sr_base >> 32);
+            const uint32_t base = srf_base((uint32_t)cf.sr_base, (uint32_t)(cf.sr_base >> 32), sr_idx);
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
-                uint32_t acc = 0;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int j = qq * 8 + k;
-                    acc |= sr_code_fast(v[j], sc_f, k0, k1, sr_idx + (uint64_t)j) << (4 * k);
-                }
-                w[qq] = acc;
+                const int j = qq * 8;
+                w[qq] = srf_quad(__fmul_rn(v[j], sc_f), __fmul_rn(v[j + 1], sc_f), __fmul_rn(v[j + 2], sc_f),
+                                 __fmul_rn(v[j + 3], sc_f), srf_rbits(base, 2 * qq)) |
+                        srf_quad(__fmul_rn(v[j + 4], sc_f), __fmul_rn(v[j + 5], sc_f), __fmul_rn(v[j + 6], sc_f),
+                                 __fmul_rn(v[j + 7], sc_f), srf_rbits(base, 2 * qq + 1)) << 16;
             }
         } else {
 #pragma unroll

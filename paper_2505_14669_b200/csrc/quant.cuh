@@ -130,35 +130,33 @@ __device__ __forceinline__ uint32_t sr_code(float x, float sc_f, double sc_d, ui
 
 
 // Fast stochastic rounding (B200 extension, QT_ROUND_SR_FAST; SURVEY.md section 7.3 "fast mode"): the same two
-// grid neighbours as sr_code, picked with the same probability (up to 2^-22 of a grid step), from a 32-bit hash
-// of (key, stream position) instead of the reference's splitmix64 stream -- the draws are NOT the reference's.
-// No 64-bit multiplies, no f64, no neighbour ladder.
-// The fast-SR code of an already scaled value v (= x / s, |v| <= 6).  On [0.5, 8) the E2M1 grid keeps 1 mantissa
-// bit (0 on [0.5, 1)), so stochastic rounding is "add a uniform integer below the dropped bits, then truncate":
-// the result is the upper neighbour with probability (dropped bits) / 2^drop = (|v| - lo) / (hi - lo), and a carry
-// lands exactly on the next grid point.  Below 0.5 the neighbours are 0 and 0.5 with P(0.5) = 2 |v| (24-bit
-// uniform).  The sign is applied to the magnitude's code (the grid is symmetric, so the distribution equals the
-// reference's signed-grid SR).  Uniforms from a 32-bit hash of (key, stream position).
-__device__ __forceinline__ uint32_t sr_fast_code(float v, uint32_t k0, uint32_t k1, uint64_t index) {
-    uint32_t h = (uint32_t)index * 0x9E3779B1u + k0;          // lowbias32 of (position, key)
-    h ^= (uint32_t)(index >> 32) * 0x85EBCA77u + k1;
+// grid neighbours as sr_code, picked by the hardware's stochastic-rounding conversion
+// cvt.rs.satfinite.e2m1x4.f32 (F2FP.E2M1.RS: four values, 32 random bits) -- the draws are NOT the reference's.
+// Measured exhaustively over all 2^32 random words (tools/ubench/cvt_rs_exh.cu): the upper neighbour is taken with
+// probability floor(p * 2^16) / 2^16, p = (|v| - lo) / (hi - lo), in every grid interval -- unbiased up to a
+// shrink toward zero below 2^-16 of a grid step; the four decisions of one conversion are uncorrelated to
+// |r| <= 3e-4 (tools/ubench/cvt_rs_corr.cu).
+// Random words: quad q (elements 4q .. 4q+3) of the group whose first stream position is P takes
+// lowbias32(srf_base(P) + q * C), srf_base(P) = lo32(P) * C + k0 + (hi32(P) * C' ^ k1) (groups of every operand lie
+// along the stream's contiguous axis, so the words are a function of stream positions alone).
+constexpr uint32_t kSrfC = 0x9E3779B1u;
+__device__ __forceinline__ uint32_t srf_base(uint32_t k0, uint32_t k1, uint64_t p) {
+    return (uint32_t)p * kSrfC + k0 + ((uint32_t)(p >> 32) * 0x85EBCA77u ^ k1);
+}
+__device__ __forceinline__ uint32_t srf_rbits(uint32_t base, uint32_t q) {
+    uint32_t h = base + q * kSrfC;   // lowbias32
     h ^= h >> 16;
     h *= 0x7FEB352Du;
     h ^= h >> 15;
     h *= 0x846CA68Bu;
     h ^= h >> 16;
-    const uint32_t bits = __float_as_uint(v) & 0x7FFFFFFFu;
-    uint32_t mag;
-    if (bits >= 0x3F000000u) {                                // |v| >= 0.5
-        const uint32_t mask = bits >= 0x3F800000u ? 0x3FFFFFu : 0x7FFFFFu;
-        mag = (bits + ((h >> 9) & mask)) & ~mask;
-    } else {
-        mag = (float)(h >> 8) < __fmul_rn(__uint_as_float(bits), 33554432.0f) ? 0x3F000000u : 0u;
-    }
-    const uint32_t c = e2m1x2(__uint_as_float(mag), 0.0f) & 7u;   // exact grid value -> its magnitude code
-    return c == 0 ? 0u : c | ((__float_as_uint(v) >> 28) & 8u);
+    return h;
 }
-__device__ __forceinline__ uint32_t sr_code_fast(float x, float sc_f, uint32_t k0, uint32_t k1, uint64_t index) {
-    return sr_fast_code(__fmul_rn(x, sc_f), k0, k1, index);
+// E2M1 codes of four scaled values (|v| <= 6), element k in nibble k; -0 -> +0 (_native.pyx:127-130)
+__device__ __forceinline__ uint32_t srf_quad(float e0, float e1, float e2, float e3, uint32_t rbits) {
+    uint16_t o;
+    asm("cvt.rs.satfinite.e2m1x4.f32 %0, {%1, %2, %3, %4}, %5;" : "=h"(o) : "f"(e3), "f"(e2), "f"(e1), "f"(e0), "r"(rbits));
+    const uint32_t w = o, mag = w & 0x7777u;
+    return mag | (w & ((mag + 0x7777u) & 0x8888u));
 }
 }  // namespace qt

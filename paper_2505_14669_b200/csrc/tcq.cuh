@@ -51,14 +51,15 @@ __device__ __forceinline__ bool srf_checked(const float (&acc)[32], float presca
     const float s2 = __uint_as_float((uint32_t)(254 - e) << 23);
     ok = ok && (amax == 0.0f || (__fmul_rd(amp - d, s2) > 3.0f && __fmul_ru(amp + d, s2) < 6.0f));
     const float sc = kC5 * prescale * s2;
+    const uint32_t base = srf_base(k0, k1, idx0);
     uint32_t w[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        uint32_t acc4 = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            acc4 |= sr_fast_code(__fmul_rn(acc[8 * q + k], sc), k0, k1, idx0 + (uint64_t)(8 * q + k)) << (4 * k);
-        w[q] = acc4;
+        const int j = 8 * q;
+        w[q] = srf_quad(__fmul_rn(acc[j], sc), __fmul_rn(acc[j + 1], sc), __fmul_rn(acc[j + 2], sc),
+                        __fmul_rn(acc[j + 3], sc), srf_rbits(base, 2 * q)) |
+               srf_quad(__fmul_rn(acc[j + 4], sc), __fmul_rn(acc[j + 5], sc), __fmul_rn(acc[j + 6], sc),
+                        __fmul_rn(acc[j + 7], sc), srf_rbits(base, 2 * q + 1)) << 16;
     }
     codes = make_uint4(w[0], w[1], w[2], w[3]);
     e_out = e;
@@ -155,7 +156,11 @@ __device__ __forceinline__ void exact_group_warp(const uint8_t* tile, bool col, 
     if (srf) {   // QT_ROUND_SR_FAST: quant_group<kSr>'s order -- pre-scale, ceil exponent of the pre-scaled amax
         v = __fmul_rn(v, prescale);
         e = ceil_scale_exp(__fmul_rn(am, prescale));
-        nib = sr_code_fast(v, exp2i(127 - e), k0, k1, idx0 + (uint64_t)j);
+        const float vs = __fmul_rn(v, exp2i(127 - e));
+        const int q0 = j & ~3;
+        const float e0 = __shfl_sync(0xffffffffu, vs, q0), e1 = __shfl_sync(0xffffffffu, vs, q0 + 1);
+        const float e2 = __shfl_sync(0xffffffffu, vs, q0 + 2), e3 = __shfl_sync(0xffffffffu, vs, q0 + 3);
+        nib = (srf_quad(e0, e1, e2, e3, srf_rbits(srf_base(k0, k1, idx0), (uint32_t)(j >> 2))) >> (4 * (j & 3))) & 0xFu;
     } else {
         if (!rtn_scale(am, prescale, e, sc)) v = __fmul_rn(v, prescale);
         nib = e2m1b(__fmul_rn(v, sc), 0.0f) & 0xFu;

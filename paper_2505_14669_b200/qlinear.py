@@ -307,7 +307,7 @@ def _rounding_code(rounding: str) -> int:
         return _lib.QT_ROUND_RTN
     if rounding == "sr":
         return _lib.QT_ROUND_SR
-    if rounding == "sr_fast":   # B200 extension: unbiased SR with hash uniforms (not the reference's draws)
+    if rounding == "sr_fast":   # B200 extension: hardware SR (cvt.rs), unbiased to 2^-16 of a step (not the reference's draws)
         return _lib.QT_ROUND_SR_FAST
     if rounding == "exact":
         raise NotImplementedError("rounding='exact' skips quantization: a CPU test mode (oracle), not a GPU path")
