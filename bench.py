@@ -413,8 +413,9 @@ def run_ours(args, rank, world, local_rank):
     if world == 1 and not args.no_graph:
         for mode, what in (("sr", "same step, backward rounding 'sr' (G, G_t, W_t, X_t by SR on the reference's "
                                   "splitmix64 stream, bit-exact)"),
-                           ("sr_fast", "same step, backward rounding 'sr_fast' (B200 extension: the same SR "
-                                       "decisions against 24-bit hash uniforms; statistically unbiased)")):
+                           ("sr_fast", "same step, backward rounding 'sr_fast' (B200 extension: SR to the same "
+                                       "neighbours by the hardware conversion cvt.rs.e2m1x4, P(up) = floor(p 2^16) / 2^16; "
+                                       "not the reference's draws)")):
             g_sr, _ = capture(lambda m=mode: step(args.warmup + 2, rounding=m))
             g_sr.replay()
             torch.cuda.synchronize()
