@@ -1,50 +1,52 @@
-"""PCIe probe: pinned H2D alone, D2H alone, and both directions at once on two streams (GB/s).
-
-Decides whether the end-to-end bench can overlap its input uploads with its result downloads.
-"""
+"""PCIe bandwidth of the e2e arm's transfers: pinned H2D alone, D2H alone, and both at once (full duplex),
+with the bench's per-step byte counts (1.258 GB in, 1.057 GB out)."""
 import torch
 
-
-def main():
-    n = 512 << 20
-    h_in = torch.empty(n, dtype=torch.uint8).pin_memory()
-    h_out = torch.empty(n, dtype=torch.uint8).pin_memory()
-    d_in = torch.empty(n, dtype=torch.uint8, device="cuda")
-    d_out = torch.empty(n, dtype=torch.uint8, device="cuda")
-    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-
-    def timed(fn, reps=5):
-        fn()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(reps):
-            fn()
-        cur = torch.cuda.current_stream()
-        cur.wait_stream(s1)
-        cur.wait_stream(s2)
-        b.record()
-        torch.cuda.synchronize()
-        return a.elapsed_time(b) / reps * 1e-3
-
-    def h2d():
-        with torch.cuda.stream(s1):
-            s1.wait_stream(torch.cuda.current_stream())
-            d_in.copy_(h_in, non_blocking=True)
-
-    def d2h():
-        with torch.cuda.stream(s2):
-            s2.wait_stream(torch.cuda.current_stream())
-            h_out.copy_(d_out, non_blocking=True)
-
-    def both():
-        h2d()
-        d2h()
-
-    t1, t2, t3 = timed(h2d), timed(d2h), timed(both)
-    print(f"H2D {n / t1 / 1e9:.1f} GB/s, D2H {n / t2 / 1e9:.1f} GB/s, "
-          f"both at once {2 * n / t3 / 1e9:.1f} GB/s aggregate ({t3 * 1e3:.2f} ms vs {(t1 + t2) * 1e3:.2f} serial)")
+dev = torch.device("cuda", 0)
+n_in, n_out = 1258291200, 1056964608
+hi = torch.empty(n_in, dtype=torch.uint8, pin_memory=True)
+ho = torch.empty(n_out, dtype=torch.uint8, pin_memory=True)
+di = torch.empty(n_in, dtype=torch.uint8, device=dev)
+do = torch.empty(n_out, dtype=torch.uint8, device=dev)
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
 
 
-if __name__ == "__main__":
-    main()
+def timed(f, reps=5):
+    f()
+    torch.cuda.synchronize()
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.record()
+    for _ in range(reps):
+        f()
+    en.record()
+    torch.cuda.synchronize()
+    return st.elapsed_time(en) / reps
+
+
+def h2d():
+    di.copy_(hi, non_blocking=True)
+
+
+def d2h():
+    ho.copy_(do, non_blocking=True)
+
+
+def both():
+    cur = torch.cuda.current_stream()
+    s1.wait_stream(cur)
+    s2.wait_stream(cur)
+    with torch.cuda.stream(s1):
+        di.copy_(hi, non_blocking=True)
+    with torch.cuda.stream(s2):
+        ho.copy_(do, non_blocking=True)
+    cur.wait_stream(s1)
+    cur.wait_stream(s2)
+
+
+t1, t2, t3 = timed(h2d), timed(d2h), timed(both)
+print(f"H2D alone {n_in / t1 / 1e6:.1f} GB/s ({t1:.2f} ms); D2H alone {n_out / t2 / 1e6:.1f} GB/s ({t2:.2f} ms); "
+      f"both at once {t3:.2f} ms (H2D-bound floor of the e2e step)")
+for mb in (8, 32, 134):
+    n = mb * 1 << 20
+    t = timed(lambda: di[:n].copy_(hi[:n], non_blocking=True), reps=20)
+    print(f"H2D chunk {mb} MiB: {n / t / 1e6:.1f} GB/s")
