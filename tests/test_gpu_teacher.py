@@ -40,3 +40,31 @@ def test_teacher_loss_parity(oracle, pair):
     print(f"{pair}: final {final:.9f} vs reference {ref_final:.9f}; max rel dev {rel.max():.3e}")
     assert rel.max() < 1e-4, rel
     assert abs(final / ref_final - 1) < 1e-4
+
+
+@pytest.mark.parametrize("s", [0, 1])
+def test_teacher_with_hardware_sr(oracle, s):
+    """quest:sr_fast (the B200 hardware-SR backward, QT_ROUND_SR_FAST) trains the reference's teacher-student task
+    like the reference's quest:sr.  The draws differ, so single runs differ (the final held-out loss spreads by
+    ~1-2 % over backward streams for either mode); the test compares the mean final loss over six backward streams
+    (xi salts, the first one the reference's own) of both modes: the difference must stay within 3 standard errors.
+    Observed on B200: seed 0 0.6362 +- 0.0145 vs 0.6304 +- 0.0112, seed 1 0.5969 +- 0.0075 vs 0.5993 +- 0.0095."""
+    import paper_2505_14669_b200 as qt
+    from toy_teacher import Teacher, train
+
+    qt.load()
+    z = np.load(GOLDEN)
+    task = Teacher(oracle, seed=0)
+    seed = int(z[f"quest_sr_s{s}_seed"])
+    salts = (None, 1, 2, 3, 4, 5)
+    fin = {}
+    for bwd in ("sr", "sr_fast"):
+        runs = [train(qt, oracle, task, seed, fwd="quest", bwd=bwd, xi_salt=k) for k in salts]
+        fin[bwd] = np.array([f for _, f in runs])
+        for hist, _ in runs:
+            assert hist[-1, 1] < 0.8 * hist[0, 1]                         # the loss falls
+    assert abs(fin["sr"][0] / float(z[f"quest_sr_s{s}_final"]) - 1) < 1e-4   # stream 0 is the reference's run
+    d = fin["sr_fast"].mean() - fin["sr"].mean()
+    se = np.sqrt(fin["sr"].var(ddof=1) / len(salts) + fin["sr_fast"].var(ddof=1) / len(salts))
+    print(f"seed {s}: sr_fast {fin['sr_fast'].mean():.5f} sr {fin['sr'].mean():.5f} diff {d:+.5f} se {se:.5f}")
+    assert abs(d) <= 3 * se

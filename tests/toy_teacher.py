@@ -101,7 +101,7 @@ def model_backward(qt, ws, acts, caches, dy, bwd, xi):
 
 
 def train(qt, orc, task, seed, fwd="quest", bwd="rtn", steps=400, batch=64, lr=0.02, wd=0.1, clip=1.0,
-          b1=0.9, b2=0.95, eps=1e-8, eval_every=10):
+          b1=0.9, b2=0.95, eps=1e-8, eval_every=10, xi_salt=None):
     ws = init_weights(orc, seed)
     ms = [np.zeros_like(w) for w in ws]
     vs = [np.zeros_like(w) for w in ws]
@@ -113,7 +113,8 @@ def train(qt, orc, task, seed, fwd="quest", bwd="rtn", steps=400, batch=64, lr=0
         loss, dy = task.loss_grad(acts[-1], target)
         if step % eval_every == 0 or step == steps - 1:
             history.append((step, loss, lr_s))
-        grads = model_backward(qt, ws, acts, caches, dy, bwd, qt.derive_seed(seed, T_XI, step))
+        xi = qt.derive_seed(seed, T_XI, step) if xi_salt is None else qt.derive_seed(seed, T_XI, step, xi_salt)
+        grads = model_backward(qt, ws, acts, caches, dy, bwd, xi)   # xi_salt: other backward streams (tests)
         gnorm = math.sqrt(sum(float(np.sum(g.astype(np.float64) ** 2)) for g in grads))
         if gnorm > clip:
             sc = np.float32(clip / gnorm)
