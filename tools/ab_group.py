@@ -1,3 +1,5 @@
+"""A/B of the shared-input group quantization: rows-only X_q + one requantization per layer vs the fused
+X_q + X_t of the first layer + requantizations of the others (nn.QuartetLinearGroupFn)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch

@@ -1,3 +1,6 @@
+"""Final held-out loss of the reference's teacher-student task over six backward streams (xi salts) for
+rtn / sr / sr_fast backward rounding: the spread that tests/test_gpu_teacher.py's hardware-SR tolerance is
+based on.  Run from the repo root on a GPU box."""
 import os, sys
 sys.path.insert(0, os.path.join(os.getcwd(), "tests")); sys.path.insert(0, os.getcwd())
 import numpy as np
