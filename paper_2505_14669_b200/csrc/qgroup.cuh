@@ -298,13 +298,14 @@ __device__ __forceinline__ int quant_group(float (&v)[32], const QuantCfg& cf, u
                                  __fmul_rn(v[j + 7], sc_f), srf_rbits(base, 2 * qq + 1)) << 16;
             }
         } else {
+            const uint64_t z0 = cf.sr_base + (sr_idx + 1) * kGolden;   // splitmix64 counter of element 0
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
                 uint32_t acc = 0;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     const int j = qq * 8 + k;
-                    acc |= sr_code(v[j], sc_f, sc_d, cf.sr_base, sr_idx + (uint64_t)j) << (4 * k);
+                    acc |= sr_code(v[j], sc_f, sc_d, z0 + (uint64_t)j * kGolden) << (4 * k);
                 }
                 w[qq] = acc;
             }

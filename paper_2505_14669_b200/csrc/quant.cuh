@@ -101,8 +101,11 @@ static __device__ __noinline__ int quest_exact_cold(const float* xs, int e_hi, i
 }
 
 // Stochastic rounding of one element (_native.pyx:156-167): v = x / s in f64, neighbours on the
-// signed grid, p = (v - lo) / (hi - lo) in f64, u = splitmix64 uniform at `index`, hi when u < p.
-__device__ __forceinline__ uint32_t sr_code(float x, float sc_f, double sc_d, uint64_t base, uint64_t index) {
+// signed grid, p = (v - lo) / (hi - lo) in f64, u = splitmix64 uniform at stream position index, hi when u < p.
+// z = base + (index + 1) * kGolden (the pre-mix counter; callers step it by kGolden per element).
+// Reference form, kept out of line: sr_code calls it for zero, tiny or non-finite scaled values only (an inlined
+// copy, or no call at all, measured slower: the rare path costs the hot loop registers and scheduling).
+static __device__ __noinline__ uint32_t sr_code_ref(float x, float sc_f, double sc_d, uint64_t z) {
     const float a = fabsf(x) * sc_f;
     int b;
     double lo;
@@ -123,11 +126,37 @@ __device__ __forceinline__ uint32_t sr_code(float x, float sc_f, double sc_d, ui
     // exact reciprocal (both are the correctly rounded value of the same real), with no double division
     const double inv_span = b < 4 ? 2.0 : (b < 6 ? 1.0 : 0.5);
     const double p = __dmul_rn(__dsub_rn(v, lo), inv_span);
-    const uint64_t h = mix64(base + (index + 1) * kGolden);
-    const double u = (double)(h >> 11) * (1.0 / 9007199254740992.0);
+    const double u = (double)(mix64(z) >> 11) * (1.0 / 9007199254740992.0);
     return u < p ? c_hi : c_lo;
 }
 
+// The same decision, branch-free and in magnitudes.  a = |x| s is exact in fp32 (a normal power-of-two
+// multiple of x); with bl = #{grid points 0.5 .. 4 <= a} and on = (a is one of them), the reference's interval
+// index is b = bl - on for x > 0 (grid(b) < a <= grid(b+1)) and b = bl for x <= 0 (grid(b) <= a < grid(b+1)),
+// read off a's exponent and top mantissa bit.  q = (a - grid(b)) / span(b) is exact in fp32 (grid(b) = 0, or
+// grid(b) <= a <= 2 grid(b): Sterbenz; the span is a power of two), and the reference's p is q (x > 0) or
+// 1 - q (x <= 0), both exact in f64: so u < p is the same comparison.  x > 0: magnitude b + [u < q];
+// x <= 0: magnitude b + [u >= 1 - q], negative sign unless the magnitude is 0.
+// 2.2x fewer instructions than the reference form (a divergent sign branch, f64 grid arithmetic).
+__device__ __forceinline__ uint32_t sr_code(float x, float sc_f, double sc_d, uint64_t z) {
+    const float a = fabsf(x) * sc_f;
+    if (!(a >= 1.0e-30f && a <= 6.0f)) return sr_code_ref(x, sc_f, sc_d, z);   // zero, tiny, non-finite
+    const uint32_t t = __float_as_uint(a);
+    const int idx = a >= 1.0f ? 2 + 2 * ((int)(t >> 23) - 127) + (int)((t >> 22) & 1u) : (a >= 0.5f ? 1 : 0);
+    const int bl = idx < 6 ? idx : 6;
+    const bool on = (a >= 1.0f && a <= 4.0f && (t & 0x3FFFFFu) == 0) || a == 0.5f;
+    const bool pos = x > 0.0f;
+    const int b = pos && on ? bl - 1 : bl;
+    const uint32_t gbits = b >= 2 ? ((uint32_t)(127 + ((b - 2) >> 1)) << 23) | ((uint32_t)((b - 2) & 1) << 22)
+                                  : (b == 1 ? 0x3F000000u : 0u);
+    const float isp = b < 4 ? 2.0f : (b < 6 ? 1.0f : 0.5f);
+    const float q = __fmul_rn(__fsub_rn(a, __uint_as_float(gbits)), isp);
+    const double qd = (double)q;
+    const double u = (double)(mix64(z) >> 11) * (1.0 / 9007199254740992.0);
+    const bool up = pos ? u < qd : !(u < 1.0 - qd);
+    const uint32_t mag = (uint32_t)b + (up ? 1u : 0u);
+    return mag == 0 ? 0u : (mag | (pos ? 0u : 8u));
+}
 
 // Fast stochastic rounding (B200 extension, QT_ROUND_SR_FAST; SURVEY.md section 7.3 "fast mode"): the same two
 // grid neighbours as sr_code, picked by the hardware's stochastic-rounding conversion
