@@ -251,7 +251,9 @@ __device__ __forceinline__ bool rtn_scale(float amax, float prescale, int& e, fl
 
 // ------------------------------------------------------------------------ group quantizer
 // Quantize one transformed group v (pre-scale NOT yet applied).  Returns the E8M0 byte.
-template <int ROUND>
+// SR_REF: exact SR by the reference form inline (sr_code_ref_body) instead of sr_code -- same codes, faster in the
+// register-heavy fused forward kernels.
+template <int ROUND, bool SR_REF = false>
 __device__ __forceinline__ int quant_group(float (&v)[32], const QuantCfg& cf, uint64_t sr_idx, int* err,
                                            int* fallbacks, uint4& codes, uint32_t& mask) {
     const float am = absmax32(v);
@@ -305,7 +307,8 @@ __device__ __forceinline__ int quant_group(float (&v)[32], const QuantCfg& cf, u
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     const int j = qq * 8 + k;
-                    acc |= sr_code(v[j], sc_f, sc_d, z0 + (uint64_t)j * kGolden) << (4 * k);
+                    const uint64_t z = z0 + (uint64_t)j * kGolden;
+                    acc |= (SR_REF ? sr_code_ref_body(v[j], sc_f, sc_d, z) : sr_code(v[j], sc_f, sc_d, z)) << (4 * k);
                 }
                 w[qq] = acc;
             }

@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(256, 2) k_quant(TileArgs a) {
                 const int64_t cld = cc.counter_ld ? cc.counter_ld : a.R;
                 uint4 codes;
                 uint32_t mask;
-                const int e = quant_group<CROUND>(v, cc, cc.counter_start + (uint64_t)(orow * cld + ogrp * 32),
+                const int e = quant_group<CROUND, ROW == kQuest>(v, cc, cc.counter_start + (uint64_t)(orow * cld + ogrp * 32),
                                                   a.col_out.err, nullptr, codes, mask);
                 *reinterpret_cast<uint4*>(a.col_out.codes + orow * a.col_out.ldc + ogrp * 16) = codes;
                 a.col_out.sf[sf_offset(orow, ogrp, a.col_out.katoms)] = (uint8_t)e;
@@ -490,9 +490,9 @@ __global__ void __launch_bounds__(256, 2) k_quant(TileArgs a) {
                 const uint64_t idx = cc.counter_start + (uint64_t)(orow * cld + ogrp * 32);
                 uint4 codes;
                 uint32_t mask;
-                const int eA = quant_group<CROUND>(va, cc, idx, a.col_out.err, nullptr, codes, mask);
+                const int eA = quant_group<CROUND, ROW == kQuest>(va, cc, idx, a.col_out.err, nullptr, codes, mask);
                 *reinterpret_cast<uint4*>(a.col_out.codes + orow * a.col_out.ldc + ogrp * 16) = codes;
-                const int eB = quant_group<CROUND>(vb, cc, idx + (uint64_t)cld, a.col_out.err, nullptr, codes, mask);
+                const int eB = quant_group<CROUND, ROW == kQuest>(vb, cc, idx + (uint64_t)cld, a.col_out.err, nullptr, codes, mask);
                 *reinterpret_cast<uint4*>(a.col_out.codes + (orow + 1) * a.col_out.ldc + ogrp * 16) = codes;
                 a.col_out.sf[sf_offset(orow, ogrp, a.col_out.katoms)] = (uint8_t)eA;
                 a.col_out.sf[sf_offset(orow + 1, ogrp, a.col_out.katoms)] = (uint8_t)eB;

@@ -103,9 +103,10 @@ static __device__ __noinline__ int quest_exact_cold(const float* xs, int e_hi, i
 // Stochastic rounding of one element (_native.pyx:156-167): v = x / s in f64, neighbours on the
 // signed grid, p = (v - lo) / (hi - lo) in f64, u = splitmix64 uniform at stream position index, hi when u < p.
 // z = base + (index + 1) * kGolden (the pre-mix counter; callers step it by kGolden per element).
-// Reference form, kept out of line: sr_code calls it for zero, tiny or non-finite scaled values only (an inlined
-// copy, or no call at all, measured slower: the rare path costs the hot loop registers and scheduling).
-static __device__ __noinline__ uint32_t sr_code_ref(float x, float sc_f, double sc_d, uint64_t z) {
+// Reference form.  sr_code calls it out of line for zero, tiny or non-finite scaled values only (an inlined copy,
+// or no call at all, measured slower: the rare path costs the hot loop registers and scheduling); the fused
+// forward kernels use it inline for their X_t / W_t (measured faster there than sr_code).
+__device__ __forceinline__ uint32_t sr_code_ref_body(float x, float sc_f, double sc_d, uint64_t z) {
     const float a = fabsf(x) * sc_f;
     int b;
     double lo;
@@ -128,6 +129,10 @@ static __device__ __noinline__ uint32_t sr_code_ref(float x, float sc_f, double 
     const double p = __dmul_rn(__dsub_rn(v, lo), inv_span);
     const double u = (double)(mix64(z) >> 11) * (1.0 / 9007199254740992.0);
     return u < p ? c_hi : c_lo;
+}
+
+static __device__ __noinline__ uint32_t sr_code_ref(float x, float sc_f, double sc_d, uint64_t z) {
+    return sr_code_ref_body(x, sc_f, sc_d, z);
 }
 
 // The same decision, branch-free and in magnitudes.  a = |x| s is exact in fp32 (a normal power-of-two
