@@ -63,17 +63,37 @@ __device__ __forceinline__ void fwht_stage1(float (&v)[32]) {
     for (int t = 0; t < 32; ++t)
         if (!(t & H)) bfly(v[t], v[t + H]);
 }
+// Stages h = H0 .. 16 with packed f32x2 arithmetic: lanes (v[i], v[i + 16]) carry two independent butterflies
+// of every stage h < 16 (pairs (t, t + h) and (t + 16, t + 16 + h)), so one FADD2 / FFMA2 does the work of two
+// scalar ops; stage 16 pairs the two lanes and stays scalar.  Same operations and order as the reference
+// (lower index as minuend, (a + b) * c and (a - b) * c rounded separately: the product is an FFMA2 with an
+// opaque -0 addend, which ptxas can neither drop nor fuse with the next add -- see opaque_nz2).
+template <int H0>
+__device__ __forceinline__ void fwht_from(float (&v)[32]) {
+    const float2 c2 = f2(kHc), nz = opaque_nz2();
+    float2 p[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) p[i] = make_float2(v[i], v[i + 16]);
+#pragma unroll
+    for (int h = H0; h < 16; h <<= 1) {
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            if (t & h) continue;
+            const float2 a = p[t], b = p[t + h];
+            p[t] = fma2(add2(a, b), c2, nz);
+            p[t + h] = fma2(sub2(a, b), c2, nz);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        v[i] = p[i].x;
+        v[i + 16] = p[i].y;
+        bfly(v[i], v[i + 16]);
+    }
+}
 // stages h = 2..16 (stage 1 is done while loading)
-__device__ __forceinline__ void fwht_tail(float (&v)[32]) {
-    fwht_stage1<2>(v);
-    fwht_stage1<4>(v);
-    fwht_stage1<8>(v);
-    fwht_stage1<16>(v);
-}
-__device__ __forceinline__ void fwht_full(float (&v)[32]) {
-    fwht_stage1<1>(v);
-    fwht_tail(v);
-}
+__device__ __forceinline__ void fwht_tail(float (&v)[32]) { fwht_from<2>(v); }
+__device__ __forceinline__ void fwht_full(float (&v)[32]) { fwht_from<1>(v); }
 
 // ------------------------------------------------------------------------------ absmax
 __device__ __forceinline__ float max3_nan(float a, float b, float c) {
