@@ -49,6 +49,7 @@ void qt_debug_set_gemm(int dbg) {
     g_gemm_dbg = dbg & 0xFFFF;
     qt::g_gemm_2sm = (dbg & 0x40000) ? 0 : 1;       // bit 18: force the 1-CTA kernel (A/B tests)
     qt::g_gemm_cluster8 = (dbg & 0x80000) ? 1 : 0;  // bit 19: clusters of 4 pairs with TMA multicast
+    qt::g_gemm_splitk = (dbg & 0x100000) ? 0 : 1;   // bit 20: no split-K for under-filled fp32 GEMMs
 }
 
 void qt_debug_set_quant(int mode, int* fallbacks) {

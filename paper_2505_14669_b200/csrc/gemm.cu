@@ -502,7 +502,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nk = (K + 255) / 256;
     const int tiles_m = (M + 255) / 256, tiles_n = (N + BN - 1) / BN;
     const int sup_m = NP == 4 ? (tiles_m + 1) / 2 : tiles_m, sup_n = NP == 4 ? (tiles_n + 1) / 2 : tiles_n;
-    const int tiles = sup_m * sup_n;                        // (super-)tiles walked by the cluster
+    // work units: (super-)tiles, each split into ks K ranges when the launcher splits K (ks = 1 or 2; the
+    // partial results are added into a zeroed fp32 output by the epilogue's TMA reduce-add)
+    const int ks = NP == 1 && ep.ksplit > 1 ? ep.ksplit : 1;
+    const int tiles = sup_m * sup_n * ks;
     const int cid = blockIdx.x / (2 * NP), ncl = gridDim.x / (2 * NP);
     // tile walk: grouped (gm row blocks per column sweep) for long K, row-major otherwise; dbg 0x1000 / 0x2000
     // force grouped-4 / grouped-16 (timing experiments)
@@ -540,13 +543,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint16_t mask_b = NP == 4 ? (uint16_t)((1u << ((pn << 2) | q)) | (1u << ((pn << 2) | 2 | q))) : 0;
         for (int tile = cid; tile < tiles; tile += ncl) {
             int mb, nb;
-            tile_mn(tile, sup_m, sup_n, mb, nb, gm);
+            tile_mn(tile / ks, sup_m, sup_n, mb, nb, gm);
             if (NP == 4) {
                 mb = 2 * mb + pm;
                 nb = 2 * nb + pn;
             }
             const int m0 = mb * 256 + 128 * (int)q, n0 = nb * BN;
-            for (int kt = 0; kt < nk; ++kt) {
+            const int kb0 = (tile % ks) * nk / ks, kb1 = (tile % ks + 1) * nk / ks;
+            for (int kt = kb0; kt < kb1; ++kt) {
                 mbar_wait(&empty[s], ph ^ 1);
                 if (elect_one()) {
                     const uint32_t fb = mapa_shared(smem_u32(&full[s]), lead_rank);
@@ -580,7 +584,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t dsb0 = make_sdesc(smem_u32(sSFB), 0, 128, kLayoutNone);
             const uint32_t id0 = idesc_mxf4(256, BN, 0, 0), id2 = idesc_mxf4(256, BN, 2, 2);
             const int my_tiles = tiles > cid ? (tiles - 1 - cid) / ncl + 1 : 0;
-            const int total = my_tiles * nk;
+            int total = 0;   // k-iterations of this cluster's units
+            for (int u = cid; u < tiles; u += ncl) total += (u % ks + 1) * nk / ks - (u % ks) * nk / ks;
             // one elected lane walks the whole issue loop: a single divergence region, every loop value uniform
             if (elect_one()) {
                 auto sf_copy = [&](uint32_t sx, uint32_t set) {
@@ -604,13 +609,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int tcount = 0; tcount < my_tiles; ++tcount) {
                     mbar_wait(tmem_empty, (tcount & 1) ^ 1);  // both CTAs' epilogues drained the accumulator
                     tc_fence_after();
-                    for (int kt = 0; kt < nk; ++kt, ++it) {
+                    const int unit = cid + tcount * ncl;
+                    const int kb0 = (unit % ks) * nk / ks, kb1 = (unit % ks + 1) * nk / ks;
+                    for (int kt = kb0; kt < kb1; ++kt, ++it) {
                         const uint64_t ad = da0 + s * (sm2::kA >> 4), bd = db0 + s * (sm2::kB >> 4);
                         const uint32_t so = (uint32_t)(it & 3) * 32;
 #pragma unroll
                         for (int j = 0; j < 4; ++j)
                             mma_mxf4_2sm(t_acc, ad + 2 * j, bd + 2 * j, (j & 1) ? id2 : id0, t_sfa + so + (j >> 1) * 4,
-                                         t_sfb + so + (j >> 1) * 8, (kt | j) != 0 ? 1u : 0u);
+                                         t_sfb + so + (j >> 1) * 8, (kt != kb0 || j != 0) ? 1u : 0u);
                         tc_commit_2sm(&empty[s], all_mask);
                         s = s + 1 == sm2::kStages ? 0u : s + 1;
                         ph ^= s == 0 ? 1u : 0u;
@@ -634,7 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int tcount = 0;
         for (int tile = cid; tile < tiles; tile += ncl, ++tcount) {
             int mb, nb;
-            tile_mn(tile, sup_m, sup_n, mb, nb, gm);
+            tile_mn(tile / ks, sup_m, sup_n, mb, nb, gm);
             if (NP == 4) {
                 mb = 2 * mb + pm;
                 nb = 2 * nb + pn;
@@ -735,6 +742,7 @@ static int make_sf_map(CUtensorMap* m, const uint8_t* sf, int64_t rows, int64_t 
 }
 
 int g_gemm_cluster8 = 0;  // 1: clusters of 4 pairs with TMA multicast (measured slower: fewer co-resident SMs)
+int g_gemm_splitk = 1;    // split-K for under-filled fp32 GEMMs (qt_debug_set_gemm bit 20 disables it)
 
 template <int NP>
 static int launch_2sm_np(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tsa, const CUtensorMap& tsb,
@@ -763,7 +771,18 @@ static int launch_2sm_np(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
         max_clusters = n;
     }
     const int64_t tm = (M + 255) / 256, tn = (N + 255) / 256;
-    const int64_t tiles = NP == 4 ? ((tm + 1) / 2) * ((tn + 1) / 2) : tm * tn;
+    int64_t tiles = NP == 4 ? ((tm + 1) / 2) * ((tn + 1) / 2) : tm * tn;
+    // Split-K for under-filled fp32 GEMMs (e.g. the 1280 x 1280 dW of the Llama-200M attention projections: 25
+    // pair tiles on 74 pairs): each tile's K halves become two work units whose results the epilogue adds into a
+    // zeroed output by TMA reduce-add.  Exactly two addends per element (0 + a + b = b + a): deterministic.
+    EpiParams epx = ep;
+    if (NP == 1 && g_gemm_splitk && !ep.out_bf16 && !ep.accumulate && 2 * tiles <= max_clusters && K >= 8 * 256) {
+        const cudaError_t z = cudaMemset2DAsync(ep.out, (size_t)(ep.ldo * 4), 0, (size_t)(N * 4), (size_t)M, st);
+        if (z != cudaSuccess) return (int)z;
+        epx.ksplit = 2;
+        epx.accumulate = 1;
+        tiles *= 2;
+    }
     int64_t clusters = tiles < max_clusters ? tiles : max_clusters;
     if (g_grid_cap > 0) clusters = std::max<int64_t>(1, std::min<int64_t>(clusters, g_grid_cap / (2 * NP)));
     cudaLaunchConfig_t cfg = {};
@@ -778,7 +797,7 @@ static int launch_2sm_np(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemm_mxf4_2sm<NP>, ta, tb, tsa, tsb, to, (int)M, (int)N, (int)K, ep);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemm_mxf4_2sm<NP>, ta, tb, tsa, tsb, to, (int)M, (int)N, (int)K, epx);
     return (int)e;
 }
 

@@ -47,6 +47,7 @@ struct EpiParams {
     float scale;
     int dbg;                 // experiment knobs (0 in production)
     int accumulate;          // D += epilogue result (rounded to D's dtype first), QT_EPI_ACCUMULATE
+    int ksplit = 1;          // 2-CTA kernel: K halves as separate work units, added into a zeroed fp32 D
 };
 
 // ---- per-device launch facts (the library serves any device of the process; no single-device caches)
@@ -85,6 +86,7 @@ int launch_tcq_dual(const void* x, int64_t ldx, int64_t R, int64_t C, const uint
                     const QuantCfg* srf_col = nullptr);
 extern int g_gemm_2sm;
 extern int g_gemm_cluster8;
+extern int g_gemm_splitk;
 int launch_gemm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, int64_t a_katoms, const uint8_t* b, int64_t ldb,
                 const uint8_t* b_sf, int64_t b_katoms, int64_t M, int64_t N, int64_t K, const EpiParams& ep,
                 cudaStream_t st);

@@ -170,3 +170,36 @@ def test_gemm_accumulate_equals_add(qt, mn, odt):
         got = base.clone()
         qt.gemm(A, B, out=got, accumulate=True, **kw)
         assert torch.equal(got, want), (mn, odt, kw)
+
+
+@pytest.mark.parametrize("shape", [(256, 256, 8192), (1280, 1280, 4096), (768, 512, 2048)])
+@pytest.mark.parametrize("epi", ["store", "maskH"])
+def test_split_k_for_underfilled_fp32_gemms(qt, oracle, shape, epi):
+    """fp32 GEMMs with fewer than half as many 2-CTA pair tiles as the chip has pairs split K in two (two work
+    units per tile, added into a zeroed output by the epilogue's TMA reduce-add; the Llama-200M attention dW
+    shape is 1280 x 1280).  Deterministic (two addends per element), within the stated tolerance of the f64
+    product, and within fp32 rounding of the unsplit kernel (qt_debug_set_gemm bit 20)."""
+    import ctypes
+
+    M, N, K = shape
+    r = np.random.default_rng(M + N + K)
+    a = r.normal(size=(M, K)).astype(np.float32)
+    b = r.normal(size=(N, K)).astype(np.float32)
+    if epi == "store":
+        _check(qt, oracle, a, b)
+    A, B = _operand(qt, a), _operand(qt, b)
+    kw = {}
+    if epi == "maskH":
+        kw = dict(mask=torch.randint(-2**31, 2**31 - 1, (M, N // 32), device="cuda", dtype=torch.int32),
+                  hadamard=True, scale=16 / 9)
+    s1 = qt.gemm(A, B, **kw)
+    s2 = qt.gemm(A, B, **kw)
+    assert torch.equal(s1, s2)
+    L = qt._lib.load()
+    L.qt_debug_set_gemm.argtypes = [ctypes.c_int]
+    L.qt_debug_set_gemm(0x100000)
+    try:
+        u = qt.gemm(A, B, **kw)
+    finally:
+        L.qt_debug_set_gemm(0)
+    assert float((s1 - u).norm() / u.norm()) < 1e-6
