@@ -353,7 +353,7 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 template <int CW>
 __device__ __forceinline__ void epi_stage(const uint32_t (&acc)[CW / 32][32], int row, int r_box, int cbase, int M,
                                           int N, const EpiParams& ep, float2 nz, const CUtensorMap* tmO, uint8_t* box,
-                                          int half, bool issuer, int y0) {
+                                          int half, bool issuer, int y0, bool accum) {
 #pragma unroll
     for (int pj = 0; pj < CW / 64; ++pj) {
         const int col0 = cbase + pj * 64;
@@ -408,7 +408,7 @@ __device__ __forceinline__ void epi_stage(const uint32_t (&acc)[CW / 32][32], in
                 fence_proxy_async_cta();
                 named_bar(1 + half, 128);
                 if (issuer && !(ep.dbg & 0x200)) {   // dbg 0x200 (timing only): no TMA stores
-                    if (ep.accumulate)
+                    if (accum)
                         tma_reduce_add_2d(tmO, box, ep.out_bf16 ? col0 : col0 + 32 * h, y0);
                     else
                         tma_store_2d(tmO, box, ep.out_bf16 ? col0 : col0 + 32 * h, y0);
@@ -471,6 +471,31 @@ __device__ __forceinline__ void tma_load_2d_2sm_mc(void* dst, const CUtensorMap*
         : "memory");
 }
 
+// Work unit u of the 2-CTA walk: units below `full` (nfull) are whole tiles; each later tile is two units, its lower
+// and upper K half.
+__device__ __forceinline__ void gemm_unit(int u, int full, int nk, int& tile, int& kb0, int& kb1) {
+    if (u < full) {
+        tile = u;
+        kb0 = 0;
+        kb1 = nk;
+    } else {
+        const int v = u - full;
+        tile = full + (v >> 1);
+        kb0 = (v & 1) ? nk / 2 : 0;
+        kb1 = (v & 1) ? nk : nk / 2;
+    }
+}
+
+// Zero the fp32 output blocks (256 x 256, clipped to M x N) of tiles first .. first + n - 1 of the 2-CTA walk.
+__global__ void __launch_bounds__(256) k_zero_tiles(float* out, int64_t ldo, int M, int N, int first, int tiles_m,
+                                                    int tiles_n, int gm) {
+    int mb, nb;
+    tile_mn(first + (int)blockIdx.x, tiles_m, tiles_n, mb, nb, gm);
+    const int c = nb * 256 + (threadIdx.x & 63) * 4;
+    for (int r = mb * 256 + (threadIdx.x >> 6); r < mb * 256 + 256 && r < M; r += 4)
+        if (c < N) *reinterpret_cast<float4*>(out + (int64_t)r * ldo + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 // NP = CTA pairs per cluster: 1 (cluster of 2) or 4 (cluster of 8: a 2 x 2 block of pair tiles whose A rows
 // are shared along N and B rows along M, each CTA loading half of its A and B boxes and multicasting them to
 // the CTA of the same role in the neighbouring pair, which halves the L2 -> SMEM bytes per FLOP)
@@ -502,10 +527,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nk = (K + 255) / 256;
     const int tiles_m = (M + 255) / 256, tiles_n = (N + BN - 1) / BN;
     const int sup_m = NP == 4 ? (tiles_m + 1) / 2 : tiles_m, sup_n = NP == 4 ? (tiles_n + 1) / 2 : tiles_n;
-    // work units: (super-)tiles, each split into ks K ranges when the launcher splits K (ks = 1 or 2; the
-    // partial results are added into a zeroed fp32 output by the epilogue's TMA reduce-add)
-    const int ks = NP == 1 && ep.ksplit > 1 ? ep.ksplit : 1;
-    const int tiles = sup_m * sup_n * ks;
+    // work units: the first `nfull` (super-)tiles whole, then the last `split` tiles as two K-half units each
+    // (gemm_unit; the launcher zeroes their output blocks and the epilogue adds by TMA reduce-add)
+    const int split = NP == 1 ? ep.split_tiles : 0;
+    const int nfull = sup_m * sup_n - split;
+    const int tiles = nfull + 2 * split;
     const int cid = blockIdx.x / (2 * NP), ncl = gridDim.x / (2 * NP);
     // tile walk: grouped (gm row blocks per column sweep) for long K, row-major otherwise; dbg 0x1000 / 0x2000
     // force grouped-4 / grouped-16 (timing experiments)
@@ -543,13 +569,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint16_t mask_b = NP == 4 ? (uint16_t)((1u << ((pn << 2) | q)) | (1u << ((pn << 2) | 2 | q))) : 0;
         for (int tile = cid; tile < tiles; tile += ncl) {
             int mb, nb;
-            tile_mn(tile / ks, sup_m, sup_n, mb, nb, gm);
+            int tl, kb0, kb1;
+            gemm_unit(tile, nfull, nk, tl, kb0, kb1);
+            tile_mn(tl, sup_m, sup_n, mb, nb, gm);
             if (NP == 4) {
                 mb = 2 * mb + pm;
                 nb = 2 * nb + pn;
             }
             const int m0 = mb * 256 + 128 * (int)q, n0 = nb * BN;
-            const int kb0 = (tile % ks) * nk / ks, kb1 = (tile % ks + 1) * nk / ks;
             for (int kt = kb0; kt < kb1; ++kt) {
                 mbar_wait(&empty[s], ph ^ 1);
                 if (elect_one()) {
@@ -585,7 +612,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t id0 = idesc_mxf4(256, BN, 0, 0), id2 = idesc_mxf4(256, BN, 2, 2);
             const int my_tiles = tiles > cid ? (tiles - 1 - cid) / ncl + 1 : 0;
             int total = 0;   // k-iterations of this cluster's units
-            for (int u = cid; u < tiles; u += ncl) total += (u % ks + 1) * nk / ks - (u % ks) * nk / ks;
+            for (int u = cid; u < tiles; u += ncl) {
+                int tl, kb0, kb1;
+                gemm_unit(u, nfull, nk, tl, kb0, kb1);
+                total += kb1 - kb0;
+            }
             // one elected lane walks the whole issue loop: a single divergence region, every loop value uniform
             if (elect_one()) {
                 auto sf_copy = [&](uint32_t sx, uint32_t set) {
@@ -609,8 +640,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int tcount = 0; tcount < my_tiles; ++tcount) {
                     mbar_wait(tmem_empty, (tcount & 1) ^ 1);  // both CTAs' epilogues drained the accumulator
                     tc_fence_after();
-                    const int unit = cid + tcount * ncl;
-                    const int kb0 = (unit % ks) * nk / ks, kb1 = (unit % ks + 1) * nk / ks;
+                    int tl, kb0, kb1;
+                    gemm_unit(cid + tcount * ncl, nfull, nk, tl, kb0, kb1);
                     for (int kt = kb0; kt < kb1; ++kt, ++it) {
                         const uint64_t ad = da0 + s * (sm2::kA >> 4), bd = db0 + s * (sm2::kB >> 4);
                         const uint32_t so = (uint32_t)(it & 3) * 32;
@@ -641,7 +672,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         int tcount = 0;
         for (int tile = cid; tile < tiles; tile += ncl, ++tcount) {
             int mb, nb;
-            tile_mn(tile / ks, sup_m, sup_n, mb, nb, gm);
+            int tl, kb0, kb1;
+            gemm_unit(tile, nfull, nk, tl, kb0, kb1);
+            tile_mn(tl, sup_m, sup_n, mb, nb, gm);
             if (NP == 4) {
                 mb = 2 * mb + pm;
                 nb = 2 * nb + pn;
@@ -659,7 +692,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(te_leader);  // the leader may start the next tile
             if (ep.dbg & 0x100) continue;                   // timing only: no epilogue math/stores
-            epi_stage<CW>(acc, row, quad * 32 + lane, cbase, M, N, ep, nz, &tmO, box, half, issuer, m0);
+            epi_stage<CW>(acc, row, quad * 32 + lane, cbase, M, N, ep, nz, &tmO, box, half, issuer, m0,
+                          ep.accumulate || tile >= nfull);
         }
         if (issuer) bulk_wait0();
     }
@@ -772,19 +806,24 @@ static int launch_2sm_np(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     }
     const int64_t tm = (M + 255) / 256, tn = (N + 255) / 256;
     int64_t tiles = NP == 4 ? ((tm + 1) / 2) * ((tn + 1) / 2) : tm * tn;
-    // Split-K for under-filled fp32 GEMMs (e.g. the 1280 x 1280 dW of the Llama-200M attention projections: 25
-    // pair tiles on 74 pairs): each tile's K halves become two work units whose results the epilogue adds into a
-    // zeroed output by TMA reduce-add.  Exactly two addends per element (0 + a + b = b + a): deterministic.
+    int64_t cl_max = max_clusters;
+    if (g_grid_cap > 0) cl_max = std::max<int64_t>(1, std::min<int64_t>(cl_max, g_grid_cap / (2 * NP)));
+    // Split-K of the last, partial wave of fp32 GEMMs: its `tail` tiles (tiles mod clusters; all tiles of an
+    // under-filled GEMM, e.g. the 25-tile 1280 x 1280 dW of the Llama-200M attention projections) run as two
+    // K-half units each, so the wave has twice the units and half the length; their output blocks are zeroed
+    // first and the epilogue adds both halves by TMA reduce-add.  Exactly two addends per element
+    // (0 + a + b = b + a): deterministic.
     EpiParams epx = ep;
-    if (NP == 1 && g_gemm_splitk && !ep.out_bf16 && !ep.accumulate && 2 * tiles <= max_clusters && K >= 8 * 256) {
-        const cudaError_t z = cudaMemset2DAsync(ep.out, (size_t)(ep.ldo * 4), 0, (size_t)(N * 4), (size_t)M, st);
-        if (z != cudaSuccess) return (int)z;
-        epx.ksplit = 2;
-        epx.accumulate = 1;
-        tiles *= 2;
+    const int64_t tail = tiles % cl_max;
+    if (NP == 1 && g_gemm_splitk && !ep.out_bf16 && !ep.accumulate && tail > 0 && 2 * tail <= cl_max &&
+        K >= 8 * 256) {
+        const int gm = (ep.dbg & 0x1000) ? 4 : (ep.dbg & 0x2000) ? 16 : (ep.dbg & 0x4000) ? 2 : (K >= 8192 ? 8 : 0);
+        k_zero_tiles<<<(unsigned)tail, 256, 0, st>>>(static_cast<float*>(ep.out), ep.ldo, (int)M, (int)N,
+                                                     (int)(tiles - tail), (int)tm, (int)tn, gm);
+        epx.split_tiles = (int)tail;
+        tiles += tail;
     }
-    int64_t clusters = tiles < max_clusters ? tiles : max_clusters;
-    if (g_grid_cap > 0) clusters = std::max<int64_t>(1, std::min<int64_t>(clusters, g_grid_cap / (2 * NP)));
+    const int64_t clusters = tiles < cl_max ? tiles : cl_max;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -47,7 +47,8 @@ struct EpiParams {
     float scale;
     int dbg;                 // experiment knobs (0 in production)
     int accumulate;          // D += epilogue result (rounded to D's dtype first), QT_EPI_ACCUMULATE
-    int ksplit = 1;          // 2-CTA kernel: K halves as separate work units, added into a zeroed fp32 D
+    int split_tiles = 0;     // 2-CTA kernel: the last split_tiles tiles of the walk run as two K-half work units each,
+                             // added into their zeroed fp32 D blocks by TMA reduce-add
 };
 
 // ---- per-device launch facts (the library serves any device of the process; no single-device caches)
