@@ -22,7 +22,8 @@ for _, name, ns in step:
     key = name.split("(")[0].replace("void ", "")
     key = ("k_gemm_mxf4" if "k_gemm" in key else "k_tcq_dual" if "k_tcq_dual" in key else
            "k_tcq_xq" if "k_tcq_xq" in key else
-           "k_quant" if "k_quant" in key else "k_signs" if "k_signs" in key else "torch/other")
+           "k_quant" if "k_quant" in key else "k_signs" if "k_signs" in key else
+           "k_zero_tiles" if "k_zero_tiles" in key else "torch/other")
     fam[key] = fam.get(key, 0.0) + ns
 total = sum(fam.values())
 with open(f"{out_dir}/{tag}_launch_shares.json", "w") as f:
