@@ -201,7 +201,9 @@ QT_API int qt_gemm_mxf4(const uint8_t* a_codes, const uint8_t* a_sf, const uint8
 
 /* Experiment hook for the GEMM mainloop studies in tools/gemm_probe.py (0 = production; bit 18 forces the
  * 1-CTA kernel where the 2-CTA pair kernel is the default, bit 19 runs the pairs in clusters of 8 with TMA
- * multicast of A and B -- both for A/B parity tests). */
+ * multicast of A and B, bit 20 turns off the split-K of the last wave of fp32 GEMMs -- all for A/B parity tests).
+ * qt_gemm_mxf4 with an fp32 output, no QT_EPI_ACCUMULATE and K >= 2048 may launch a second kernel (zero-fill of
+ * the split tiles' output blocks) on the same stream. */
 QT_API void qt_debug_set_gemm(int dbg);
 /* Quantizer path selection for A/B parity tests: mode 0 (production; 3 is an alias) runs the tensor-core
  * Hadamard quantizers where they apply -- the backward dual operands (bf16, RTN, randomized) and the bf16 QuEST
