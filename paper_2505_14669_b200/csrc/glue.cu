@@ -209,71 +209,83 @@ __device__ __forceinline__ void ce_merge(float& m, float& s, float m2, float s2)
     s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
     m = mn;
 }
-__global__ void k_xent(const uint4* __restrict__ logits, const int64_t* __restrict__ tgt, float* __restrict__ lse,
-                       float* __restrict__ loss, uint4* __restrict__ dlogits, const float* __restrict__ dloss,
-                       float scale, int64_t rows, int V, int backward) {
-    __shared__ float sm[32], ss[32];
+// Forward: one warp per row, online log-sum-exp; four independent 16-byte loads per lane and iteration
+// (memory-level parallelism) and one merge per 32 values (out-of-range chunks read as -inf, adding nothing);
+// shuffle-only reduction (no block barrier per row).
+__global__ void __launch_bounds__(256) k_xent_fwd(const uint4* __restrict__ logits, const int64_t* __restrict__ tgt,
+                                                  float* __restrict__ lse, float* __restrict__ loss, int64_t rows,
+                                                  int V) {
+    const int V8 = V / 8, lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
+        const uint4* row = logits + r * V8;
+        float m = -INFINITY, sum = 0.f;
+        for (int i0 = lane; i0 < V8; i0 += 4 * 32) {
+            uint4 c[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + 32 * u;
+                c[u] = i < V8 ? row[i] : make_uint4(0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u, 0xFF80FF80u);
+            }
+            float v[32], cm = -INFINITY;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t w[4] = {c[u].x, c[u].y, c[u].z, c[u].w};
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    v[8 * u + k] = bf(w[k >> 1], k & 1);
+                    cm = fmaxf(cm, v[8 * u + k]);
+                }
+            }
+            float cs = 0.f;
+            if (cm != -INFINITY) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k) cs += __expf(v[k] - cm);
+            }
+            ce_merge(m, sum, cm, cs);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+            ce_merge(m, sum, m2, s2);
+        }
+        if (lane == 0) {
+            const float l = m + __logf(sum);
+            lse[r] = l;
+            const int64_t t = tgt[r];
+            if (t >= 0 && t < V) {   // otherwise ignored (loss 0, gradient 0), like ignore_index
+                const uint32_t tw = reinterpret_cast<const uint32_t*>(row)[t >> 1];
+                loss[r] = l - bf(tw, (int)(t & 1));
+            } else {
+                loss[r] = 0.f;
+            }
+        }
+    }
+}
+
+// Backward: dlogits = (softmax - onehot) * dloss * scale, one block per row (streaming).
+__global__ void k_xent_bwd(const uint4* __restrict__ logits, const int64_t* __restrict__ tgt,
+                           const float* __restrict__ lse, uint4* __restrict__ dlogits, const float* __restrict__ dloss,
+                           float scale, int64_t rows, int V) {
     const int V8 = V / 8;
     for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
         const uint4* row = logits + r * V8;
         const int64_t t = tgt[r];
         const bool valid = t >= 0 && t < V;   // otherwise ignored (loss 0, gradient 0), like ignore_index
-        if (!backward) {
-            float m = -INFINITY, sum = 0.f;
-            for (int i = threadIdx.x; i < V8; i += blockDim.x) {
-                const uint4 c = row[i];
-                const uint32_t w[4] = {c.x, c.y, c.z, c.w};
-                float v[8], cm = -INFINITY;
+        const float l = lse[r], g = valid ? *dloss * scale : 0.f;
+        uint4* drow = dlogits + r * V8;
+        for (int i = threadIdx.x; i < V8; i += blockDim.x) {
+            const uint4 c = row[i];
+            const uint32_t w[4] = {c.x, c.y, c.z, c.w};
+            uint32_t o[4];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    v[k] = bf(w[k >> 1], k & 1);
-                    cm = fmaxf(cm, v[k]);
-                }
-                float cs = 0.f;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) cs += __expf(v[k] - cm);
-                ce_merge(m, sum, cm, cs);
+            for (int k = 0; k < 4; ++k) {
+                const int64_t j0 = (int64_t)i * 8 + 2 * k;
+                const float p0 = __expf(bf(w[k], 0) - l) - (j0 == t ? 1.f : 0.f);
+                const float p1 = __expf(bf(w[k], 1) - l) - (j0 + 1 == t ? 1.f : 0.f);
+                o[k] = pack_bf2(p0 * g, p1 * g);
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
-                ce_merge(m, sum, m2, s2);
-            }
-            const int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-            if ((threadIdx.x & 31) == 0) {
-                sm[wid] = m;
-                ss[wid] = sum;
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                float M = sm[0], S = ss[0];
-                for (int k = 1; k < nw; ++k) ce_merge(M, S, sm[k], ss[k]);
-                const float l = M + __logf(S);
-                lse[r] = l;
-                if (valid) {
-                    const uint32_t tw = reinterpret_cast<const uint32_t*>(row)[t >> 1];
-                    loss[r] = l - bf(tw, (int)(t & 1));
-                } else {
-                    loss[r] = 0.f;
-                }
-            }
-            __syncthreads();
-        } else {
-            const float l = lse[r], g = valid ? *dloss * scale : 0.f;
-            uint4* drow = dlogits + r * V8;
-            for (int i = threadIdx.x; i < V8; i += blockDim.x) {
-                const uint4 c = row[i];
-                const uint32_t w[4] = {c.x, c.y, c.z, c.w};
-                uint32_t o[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int64_t j0 = (int64_t)i * 8 + 2 * k;
-                    const float p0 = __expf(bf(w[k], 0) - l) - (j0 == t ? 1.f : 0.f);
-                    const float p1 = __expf(bf(w[k], 1) - l) - (j0 + 1 == t ? 1.f : 0.f);
-                    o[k] = pack_bf2(p0 * g, p1 * g);
-                }
-                drow[i] = make_uint4(o[0], o[1], o[2], o[3]);
-            }
+            drow[i] = make_uint4(o[0], o[1], o[2], o[3]);
         }
     }
 }
@@ -438,10 +450,17 @@ QT_API int qt_cross_entropy(const void* logits, const int64_t* targets, int64_t 
     if (!al16(logits) || (backward && !al16(dlogits))) return QT_ERR_ALIGN;
     if (rows == 0) return 0;
     const int64_t sms = qt::device_sms();
-    const int64_t blocks = rows < (int64_t)sms * 8 ? rows : (int64_t)sms * 8;
-    k_xent<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint4*>(logits), targets, lse, loss,
-                                                               static_cast<uint4*>(dlogits), dloss, scale, rows,
-                                                               vocab, backward);
+    if (!backward) {
+        const int64_t wb = (rows + 7) / 8;   // 8 rows (warps) per block
+        const int64_t blocks = wb < (int64_t)sms * 8 ? wb : (int64_t)sms * 8;
+        k_xent_fwd<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint4*>(logits), targets,
+                                                                        lse, loss, rows, vocab);
+    } else {
+        const int64_t blocks = rows < (int64_t)sms * 8 ? rows : (int64_t)sms * 8;
+        k_xent_bwd<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint4*>(logits), targets,
+                                                                        lse, static_cast<uint4*>(dlogits), dloss,
+                                                                        scale, rows, vocab);
+    }
     return (int)cudaGetLastError();
 }
 
