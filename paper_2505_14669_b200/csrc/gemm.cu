@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------- host side
-int g_gemm_2sm = 1;  // use the 2-CTA kernel where eligible (N % 256 == 0, M >= 256); 0: 1-CTA kernel only
+int g_gemm_2sm = 1;  // use the 2-CTA kernel where eligible (launch_gemm); 0: 1-CTA kernel only
 
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -875,7 +875,14 @@ int launch_gemm(const uint8_t* a, int64_t lda, const uint8_t* a_sf, int64_t a_ka
                 cudaStream_t st) {
     if (M == 0 || N == 0) return 0;
     const int esz = ep.out_bf16 ? 2 : 4;
-    if (g_gemm_2sm && N % 256 == 0 && M >= 256 && (reinterpret_cast<uintptr_t>(ep.out) & 15) == 0 &&
+    // N % 256 == 128 also runs on the pair kernel when K >= 4096: a half-filled last column tile leaves the
+    // second CTA's B box entirely past N (TMA zero fill, complete_tx still counts the full box), its B scale
+    // atoms in the zeroed 256-row padding of the scale buffer (qt_sf_bytes), and its output columns clipped by
+    // the store map -- the same situation as the half-filled last row tile of M % 256 == 128.  Measured at the
+    // Llama-30M shapes (d = 640, tools/gemm_30m_probe.py): long-K GEMMs gain (LM-head dx / dW 384 / 408 ->
+    // 286 / 287 us, ffn dW 57 -> 48 us), short-K ones (K = 640 / 1792) lose 7-20 % to the wasted half tile.
+    const bool pair_n = N % 256 == 0 || (N % 128 == 0 && K >= 4096);
+    if (g_gemm_2sm && pair_n && M >= 256 && (reinterpret_cast<uintptr_t>(ep.out) & 15) == 0 &&
         (ep.ldo * esz) % 16 == 0)
         return launch_gemm_2sm(a, lda, a_sf, a_katoms, b, ldb, b_sf, b_katoms, M, N, K, ep, st);
     if (N >= 256 && N % 256 == 0)

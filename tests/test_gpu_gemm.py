@@ -205,3 +205,38 @@ def test_split_k_for_underfilled_fp32_gemms(qt, oracle, shape, epi):
     finally:
         L.qt_debug_set_gemm(0)
     assert float((s1 - u).norm() / u.norm()) < 1e-6
+
+
+@pytest.mark.parametrize("mnk", [(640, 640, 4096), (512, 384, 4096), (1024, 128, 4352), (768, 640, 8192)])
+def test_gemm_2cta_half_column_tile(qt, oracle, mnk):
+    """N % 256 == 128 with K >= 4096 runs on the 2-CTA pair kernel: the last column tile's second-CTA B box lies
+    wholly past N (TMA zero fill; its scale atoms in the zeroed 256-row padding) and its columns are clipped by the
+    store map.
+    Matches the oracle like every other path (the fp32 shapes also take the split-K tail)."""
+    test_gemm_random(qt, oracle, mnk)
+
+
+@pytest.mark.parametrize("odt", [torch.bfloat16, torch.float32])
+def test_gemm_2cta_half_column_tile_epilogues(qt, odt):
+    """Masked FWHT . 16/9 epilogue and accumulate on a N % 256 == 128 shape: the 2-CTA result equals the 1-CTA
+    kernel's within fp32 rounding, and accumulate equals out + gemm."""
+    from paper_2505_14669_b200 import _lib
+
+    M, N, K = 768, 640, 4096
+    g = torch.Generator(device="cuda").manual_seed(7)
+    A = qt.quant_rows(torch.randn(M, K, device="cuda", generator=g), _lib.QT_TRANSFORM_NONE, _lib.QT_ROUND_RTN)
+    B = qt.quant_rows(torch.randn(N, K, device="cuda", generator=g), _lib.QT_TRANSFORM_NONE, _lib.QT_ROUND_RTN)
+    mask = torch.randint(-2**31, 2**31 - 1, (M, N // 32), device="cuda", dtype=torch.int32, generator=g)
+    two = qt.gemm(A, B, mask=mask, hadamard=True, scale=16 / 9, out_dtype=odt)
+    L = _lib.load()
+    L.qt_debug_set_gemm(0x40000)
+    try:
+        one = qt.gemm(A, B, mask=mask, hadamard=True, scale=16 / 9, out_dtype=odt)
+    finally:
+        L.qt_debug_set_gemm(0)
+    tol = 1e-5 if odt == torch.float32 else 1e-2
+    assert torch.allclose(two.float(), one.float(), rtol=tol, atol=tol * float(one.float().abs().max()))
+    base = torch.randn(M, N, device="cuda", generator=g).to(odt)
+    out = base.clone()
+    qt.gemm(A, B, out=out, accumulate=True)
+    assert torch.equal(out, base + qt.gemm(A, B, out_dtype=odt))

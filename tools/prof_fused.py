@@ -5,7 +5,9 @@ import torch
 import paper_2505_14669_b200 as qt
 from paper_2505_14669_b200 import _lib
 from paper_2505_14669_b200.mxfp4 import quant_fused, sign_bits
-qt.load()
+L = qt.load()
+if os.environ.get("QT_PROF_QMODE"):  # e.g. 51 = tensor-core path, skeleton only (tools/fwd_probe.py)
+    L.qt_debug_set_quant(int(os.environ["QT_PROF_QMODE"]), None)
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 dt = torch.float32 if len(sys.argv) > 2 and sys.argv[2] == "f32" else torch.bfloat16
 x = torch.randn(16384 if dt == torch.bfloat16 else 4096, d, device="cuda").to(dt)
