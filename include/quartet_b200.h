@@ -253,12 +253,17 @@ QT_API int qt_seam_row_sums(const double* a, const double* b, int op, int64_t ro
  * qt_swiglu: forward out0 = silu(gate) * up; backward (dy given) out0 = d gate, out1 = d up.  n % 8 == 0.
  * qt_rmsnorm: rows of x [rows, d] bf16 (d % 8 == 0 up to 2048, or d in {4096, 6144, 8192}), fp32 weight w: forward out = x rstd w and
  *   rstd[rows] saved; backward (dy, rstd given) out = dx, dw[d] += sum over rows (caller zeroes dw).
+ * qt_rmsnorm_res: qt_rmsnorm fused with the residual stream around it (bf16 sums rounded once, as torch's add):
+ *   forward h_out = x + res and out = rmsnorm(h_out); backward out = dx + res (res = the gradient that reaches
+ *   the residual stream past the norm, so autograd needs no separate accumulation).  res == NULL: qt_rmsnorm.
  * qt_cross_entropy: rows of logits [rows, vocab] bf16 (vocab % 8 == 0), int64 targets: forward writes lse and
  *   the per-row loss (fp32); backward writes dlogits = (softmax - onehot) * (*dloss) * scale (bf16). */
 QT_API int qt_rope(const void* x, void* out, int64_t rows, int heads, int head_dim, int seq, const void* cos,
                    const void* sin, int backward, int64_t stride_b, int64_t stride_s, int64_t stride_h, void* stream);
 QT_API int qt_rmsnorm(const void* x, const float* w, const void* dy, void* out, float* rstd, float* dw, int64_t rows,
                       int d, float eps, int backward, void* stream);
+QT_API int qt_rmsnorm_res(const void* x, const void* res, const float* w, const void* dy, void* out, void* h_out,
+                          float* rstd, float* dw, int64_t rows, int d, float eps, int backward, void* stream);
 QT_API int qt_cross_entropy(const void* logits, const int64_t* targets, int64_t rows, int vocab, float* lse,
                             float* loss, void* dlogits, const float* dloss, float scale, int backward, void* stream);
 QT_API int qt_swiglu(const void* gate, const void* up, const void* dy, void* out0, void* out1, int64_t n,

@@ -42,6 +42,7 @@ SIGNATURES = {
     "qt_swiglu": (_i32, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _vp]),
     "qt_cross_entropy": (_i32, [_vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _f32, _i32, _vp]),
     "qt_rmsnorm": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _f32, _i32, _vp]),
+    "qt_rmsnorm_res": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _f32, _i32, _vp]),
     "qt_seam_quantize": (_i32, [_vp, _i64, _i64, _i64, _i32, _i32, _u64, _u64, ctypes.c_double, _vp, _vp, _vp, _vp,
                                 _vp]),
     "qt_seam_fwht": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp]),

@@ -18,6 +18,14 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
     __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
     return *reinterpret_cast<uint32_t*>(&b);
 }
+// 8 bf16 + 8 bf16, each sum in fp32 rounded once to bf16 (what torch's bf16 add computes)
+__device__ __forceinline__ uint4 add_bf8(uint4 a, uint4 b) {
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) o[t] = pack_bf2(bf(aw[t], 0) + bf(bw[t], 0), bf(aw[t], 1) + bf(bw[t], 1));
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
 
 // Half-split (GPT-NeoX) rotary embedding on x [rows = B*S, H, dh] (row r at sequence position r % S),
 // tables cos/sin [S, dh].  Each thread rotates 8 (j, j + dh/2) pairs.  Backward applies the transposed
@@ -107,40 +115,58 @@ __global__ void k_swiglu(const uint4* __restrict__ g, const uint4* __restrict__ 
 
 // RMSNorm over rows of x [rows, d] bf16 with an fp32 weight, one warp per row (d % 8 == 0, d <= 2048):
 // forward y = x * rstd * w (rstd = 1/sqrt(mean(x^2) + eps) in fp32, saved); backward dx = rstd (g - xh mean(g xh))
-// with g = dy * w, xh = x * rstd, and dw += sum_rows dy * xh (per-warp partials -> smem -> one atomic per
+// with g = dy * w, xh = x * rstd, and dw += sum_rows dy * xh (per-warp partials in shared memory -> one atomic per
 // column per block).  Lane `lane` owns the 16-byte chunks v * 32 + lane (v < NV) that lie inside the row.
+// Optional residual stream (qt_rmsnorm_res): forward normalises h = x + res and writes h; backward adds res to dx.
+// Kept lean in registers (rows held as packed bf16, w re-read through L1, dw partials in shared memory) so that
+// 2-4 blocks of 8 warps fit per SM (no spills): one row per warp is a full memory round trip, and with 16-32 warps the
+// loads of many rows overlap (at 8 resident warps the kernel was latency-bound at 2-3 TB/s).
+__device__ __forceinline__ void w8(const float* __restrict__ w, int chunk, float (&o)[8]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(w) + 2 * chunk);
+    const float4 b = __ldg(reinterpret_cast<const float4*>(w) + 2 * chunk + 1);
+    o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+}
 template <int NV>  // uint4 chunks of 8 bf16 per lane: d <= 256 * NV
-__global__ void k_rmsnorm(const uint4* __restrict__ x, const float* __restrict__ w, const uint4* __restrict__ dy,
-                          uint4* __restrict__ out, float* __restrict__ rstd_io, float* __restrict__ dw, int64_t rows,
-                          int d, float eps, int backward) {
+__global__ void __launch_bounds__(256, NV <= 2 ? 4 : 2) k_rmsnorm(const uint4* __restrict__ x, const float* __restrict__ w,
+                                                    const uint4* __restrict__ dy, uint4* __restrict__ out,
+                                                    float* __restrict__ rstd_io, float* __restrict__ dw, int64_t rows,
+                                                    int d, float eps, int backward, const uint4* __restrict__ res,
+                                                    uint4* __restrict__ h_out) {
     extern __shared__ float red[];  // [warps][d] partial dw (backward)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nch = d / 8;          // chunks per row
-    float wv[NV][8];
+    float* my = red + wib * d;
+    if (backward) {
 #pragma unroll
-    for (int v = 0; v < NV; ++v)
+        for (int v = 0; v < NV; ++v)
+            if (v * 32 + lane < nch)
 #pragma unroll
-        for (int t = 0; t < 8; ++t) wv[v][t] = v * 32 + lane < nch ? w[(v * 32 + lane) * 8 + t] : 0.f;
-    float dwp[NV][8];
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int t = 0; t < 8; ++t) dwp[v][t] = 0.f;
+                for (int t = 0; t < 8; ++t) my[(v * 32 + lane) * 8 + t] = 0.f;
+    }
     for (int64_t r = (int64_t)blockIdx.x * nw + wib; r < rows; r += (int64_t)gridDim.x * nw) {
-        float xv[NV][8];
-        float ss = 0.f;
+        uint4 cx[NV], cd[NV], cr[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             const bool ok = v * 32 + lane < nch;
-            const uint4 c = ok ? x[r * nch + v * 32 + lane] : make_uint4(0, 0, 0, 0);
-            const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                xv[v][t] = bf(cw[t >> 1], t & 1);
-                ss = fmaf(xv[v][t], xv[v][t], ss);
-            }
+            cx[v] = ok ? x[r * nch + v * 32 + lane] : make_uint4(0, 0, 0, 0);
+            if (res) cr[v] = ok ? res[r * nch + v * 32 + lane] : make_uint4(0, 0, 0, 0);
+            if (backward) cd[v] = ok ? dy[r * nch + v * 32 + lane] : make_uint4(0, 0, 0, 0);
         }
         if (!backward) {
+            if (res) {   // fused residual add: h = bf16(x + y), normalised and written
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    cx[v] = add_bf8(cx[v], cr[v]);
+                    if (v * 32 + lane < nch) h_out[r * nch + v * 32 + lane] = cx[v];
+                }
+            }
+            float ss = 0.f;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const uint32_t cw[4] = {cx[v].x, cx[v].y, cx[v].z, cx[v].w};
+#pragma unroll
+                for (int t = 0; t < 8; ++t) ss = fmaf(bf(cw[t >> 1], t & 1), bf(cw[t >> 1], t & 1), ss);
+            }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
             const float rs = rsqrtf(ss / (float)d + eps);
@@ -148,27 +174,36 @@ __global__ void k_rmsnorm(const uint4* __restrict__ x, const float* __restrict__
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 if (v * 32 + lane >= nch) continue;
+                float wv[8];
+                w8(w, v * 32 + lane, wv);
+                const uint32_t cw[4] = {cx[v].x, cx[v].y, cx[v].z, cx[v].w};
                 uint32_t o4[4];
 #pragma unroll
                 for (int t = 0; t < 4; ++t)
-                    o4[t] = pack_bf2(xv[v][2 * t] * rs * wv[v][2 * t], xv[v][2 * t + 1] * rs * wv[v][2 * t + 1]);
+                    o4[t] = pack_bf2(bf(cw[t], 0) * rs * wv[2 * t], bf(cw[t], 1) * rs * wv[2 * t + 1]);
                 out[r * nch + v * 32 + lane] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
             }
         } else {
             const float rs = rstd_io[r];
-            float gv[NV][8], dot = 0.f;
+            float dot = 0.f;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-                const bool ok = v * 32 + lane < nch;
-                const uint4 c = ok ? dy[r * nch + v * 32 + lane] : make_uint4(0, 0, 0, 0);
-                const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+                if (v * 32 + lane >= nch) continue;
+                float wv[8];
+                w8(w, v * 32 + lane, wv);
+                const uint32_t xw[4] = {cx[v].x, cx[v].y, cx[v].z, cx[v].w};
+                const uint32_t dw4[4] = {cd[v].x, cd[v].y, cd[v].z, cd[v].w};
+                float* pp = my + (v * 32 + lane) * 8;
+                float4 p0 = *reinterpret_cast<float4*>(pp), p1 = *reinterpret_cast<float4*>(pp + 4);
+                float pv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
 #pragma unroll
                 for (int t = 0; t < 8; ++t) {
-                    const float dd = bf(cw[t >> 1], t & 1), xh = xv[v][t] * rs;
-                    gv[v][t] = dd * wv[v][t];
-                    dot = fmaf(gv[v][t], xh, dot);
-                    dwp[v][t] = fmaf(dd, xh, dwp[v][t]);
+                    const float dd = bf(dw4[t >> 1], t & 1), xh = bf(xw[t >> 1], t & 1) * rs;
+                    dot = fmaf(dd * wv[t], xh, dot);
+                    pv[t] = fmaf(dd, xh, pv[t]);
                 }
+                *reinterpret_cast<float4*>(pp) = make_float4(pv[0], pv[1], pv[2], pv[3]);
+                *reinterpret_cast<float4*>(pp + 4) = make_float4(pv[4], pv[5], pv[6], pv[7]);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
@@ -176,22 +211,22 @@ __global__ void k_rmsnorm(const uint4* __restrict__ x, const float* __restrict__
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 if (v * 32 + lane >= nch) continue;
+                float wv[8];
+                w8(w, v * 32 + lane, wv);
+                const uint32_t xw[4] = {cx[v].x, cx[v].y, cx[v].z, cx[v].w};
+                const uint32_t dw4[4] = {cd[v].x, cd[v].y, cd[v].z, cd[v].w};
                 uint32_t o4[4];
 #pragma unroll
                 for (int t = 0; t < 4; ++t)
-                    o4[t] = pack_bf2(rs * (gv[v][2 * t] - xv[v][2 * t] * rs * mdot),
-                                     rs * (gv[v][2 * t + 1] - xv[v][2 * t + 1] * rs * mdot));
-                out[r * nch + v * 32 + lane] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+                    o4[t] = pack_bf2(rs * (bf(dw4[t], 0) * wv[2 * t] - bf(xw[t], 0) * rs * mdot),
+                                     rs * (bf(dw4[t], 1) * wv[2 * t + 1] - bf(xw[t], 1) * rs * mdot));
+                uint4 o = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+                if (res) o = add_bf8(o, cr[v]);   // + the residual stream's gradient
+                out[r * nch + v * 32 + lane] = o;
             }
         }
     }
     if (backward) {
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            if (v * 32 + lane >= nch) continue;
-#pragma unroll
-            for (int t = 0; t < 8; ++t) red[wib * d + (v * 32 + lane) * 8 + t] = dwp[v][t];
-        }
         __syncthreads();
         for (int c = threadIdx.x; c < d; c += blockDim.x) {
             float sum = 0.f;
@@ -296,7 +331,8 @@ template <int NV>
 __global__ void __launch_bounds__(256) k_rmsnorm_wide(const uint4* __restrict__ x, const float* __restrict__ w,
                                                       const uint4* __restrict__ dy, uint4* __restrict__ out,
                                                       float* __restrict__ rstd_io, float* __restrict__ dw,
-                                                      int64_t rows, float eps, int backward) {
+                                                      int64_t rows, float eps, int backward,
+                                                      const uint4* __restrict__ res, uint4* __restrict__ h_out) {
     constexpr int D = 2048 * NV;
     __shared__ float red[8];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -323,7 +359,11 @@ __global__ void __launch_bounds__(256) k_rmsnorm_wide(const uint4* __restrict__ 
         float xv[NV][8], ss = 0.f;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-            const uint4 c = x[r * (D / 8) + v * 256 + tid];
+            uint4 c = x[r * (D / 8) + v * 256 + tid];
+            if (!backward && res) {
+                c = add_bf8(c, res[r * (D / 8) + v * 256 + tid]);
+                h_out[r * (D / 8) + v * 256 + tid] = c;
+            }
             const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
@@ -365,7 +405,9 @@ __global__ void __launch_bounds__(256) k_rmsnorm_wide(const uint4* __restrict__ 
                 for (int t = 0; t < 4; ++t)
                     o4[t] = pack_bf2(rs * (gv[v][2 * t] - xv[v][2 * t] * rs * mdot),
                                      rs * (gv[v][2 * t + 1] - xv[v][2 * t + 1] * rs * mdot));
-                out[r * (D / 8) + v * 256 + tid] = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+                uint4 o = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+                if (res) o = add_bf8(o, res[r * (D / 8) + v * 256 + tid]);
+                out[r * (D / 8) + v * 256 + tid] = o;
             }
         }
     }
@@ -404,15 +446,22 @@ QT_API int qt_rope(const void* x, void* out, int64_t rows, int heads, int head_d
 
 QT_API int qt_rmsnorm(const void* x, const float* w, const void* dy, void* out, float* rstd, float* dw, int64_t rows,
                       int d, float eps, int backward, void* stream) {
+    return qt_rmsnorm_res(x, nullptr, w, dy, out, nullptr, rstd, dw, rows, d, eps, backward, stream);
+}
+
+QT_API int qt_rmsnorm_res(const void* x, const void* res, const float* w, const void* dy, void* out, void* h_out,
+                          float* rstd, float* dw, int64_t rows, int d, float eps, int backward, void* stream) {
     if (rows < 0 || d % 8 != 0 || d < 8 || (d > 2048 && (d % 2048 != 0 || d > 8192))) return QT_ERR_SHAPE;
     if (!al16(x) || !al16(out) || (backward && (!al16(dy) || !dw))) return QT_ERR_ALIGN;
+    if (res && (!al16(res) || (!backward && (!h_out || !al16(h_out))))) return QT_ERR_ALIGN;
     if (rows == 0) return 0;
     if (d > 2048) {
         int blocks = grid_for(rows * 256);
         if (blocks > 1184) blocks = 1184;
         auto wide = [&](auto kern) {
             kern<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint4*>(x), w, static_cast<const uint4*>(dy),
-                                                           static_cast<uint4*>(out), rstd, dw, rows, eps, backward);
+                                                           static_cast<uint4*>(out), rstd, dw, rows, eps, backward,
+                                                           static_cast<const uint4*>(res), static_cast<uint4*>(h_out));
         };
         switch (d / 2048) {
             case 2: wide(k_rmsnorm_wide<2>); break;
@@ -429,7 +478,8 @@ QT_API int qt_rmsnorm(const void* x, const float* w, const void* dy, void* out, 
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<blocks, warps * 32, smem, (cudaStream_t)stream>>>(static_cast<const uint4*>(x), w,
                                                                static_cast<const uint4*>(dy), static_cast<uint4*>(out),
-                                                               rstd, dw, rows, d, eps, backward);
+                                                               rstd, dw, rows, d, eps, backward,
+                                                               static_cast<const uint4*>(res), static_cast<uint4*>(h_out));
     };
     switch ((d + 255) / 256) {
         case 1: go(k_rmsnorm<1>); break;

@@ -74,9 +74,70 @@ class RMSNorm(torch.nn.Module):
 
     def forward(self, x):  # bf16 in / out, fp32 statistics and weight
         d = x.shape[-1]
-        if d % 8 == 0 and (d <= 2048 or (d % 2048 == 0 and d <= 8192)):  # csrc/glue.cu, one pass each way
+        if _fused_norm_ok(d):  # csrc/glue.cu, one pass each way
             return _RMSNormFn.apply(x.to(torch.bfloat16), self.weight, self.eps)
         return F.rms_norm(x.to(torch.bfloat16), (d,), self.weight.to(torch.bfloat16), self.eps)
+
+
+def _fused_norm_ok(d: int) -> bool:
+    return d % 8 == 0 and (d <= 2048 or (d % 2048 == 0 and d <= 8192))
+
+
+class _AddRMSNormFn(torch.autograd.Function):
+    """(h, n) = (x + y, rmsnorm(x + y)) in one pass (y None: h = x passed through).  Backward gets the gradients of
+    both outputs and returns dx = dh + rmsnorm'(dn) from one kernel (qt_rmsnorm_res), so the residual stream's two
+    consumers need no separate gradient accumulation.  Bit-identical to `h = x + y; n = norm(h)` with autograd's
+    bf16 accumulation (each sum is rounded once to bf16, as torch's add)."""
+
+    @staticmethod
+    def forward(ctx, x, y, w, eps):
+        x2 = x.contiguous().view(-1, x.shape[-1])
+        n = torch.empty_like(x2)
+        rstd = torch.empty(x2.shape[0], dtype=torch.float32, device=x.device)
+        if y is None:
+            h = x2
+            rc = _lib.load().qt_rmsnorm(x2.data_ptr(), w.data_ptr(), None, n.data_ptr(), rstd.data_ptr(), None,
+                                        x2.shape[0], x2.shape[1], float(eps), 0, _stream(x.device))
+        else:
+            y2 = y.contiguous().view(x2.shape)
+            h = torch.empty_like(x2)
+            rc = _lib.load().qt_rmsnorm_res(x2.data_ptr(), y2.data_ptr(), w.data_ptr(), None, n.data_ptr(),
+                                            h.data_ptr(), rstd.data_ptr(), None, x2.shape[0], x2.shape[1], float(eps),
+                                            0, _stream(x.device))
+        _lib.check(rc, "qt_rmsnorm_res")
+        ctx.save_for_backward(h, w, rstd)
+        ctx.eps = eps
+        ctx.has_y = y is not None
+        h_out = h.view(x.shape) if y is not None else x.view_as(x)
+        return h_out, n.view(x.shape)
+
+    @staticmethod
+    def backward(ctx, dh, dn):
+        h2, w, rstd = ctx.saved_tensors
+        dw = torch.zeros(h2.shape[1], dtype=torch.float32, device=h2.device)
+        if dn is None:
+            dx = dh.contiguous().view(h2.shape)
+        else:
+            dn2 = dn.contiguous().view(h2.shape)
+            dx = torch.empty_like(h2)
+            res = None if dh is None else dh.contiguous().view(h2.shape)
+            _lib.check(_lib.load().qt_rmsnorm_res(h2.data_ptr(), None if res is None else res.data_ptr(), w.data_ptr(),
+                                                  dn2.data_ptr(), dx.data_ptr(), None, rstd.data_ptr(), dw.data_ptr(),
+                                                  h2.shape[0], h2.shape[1], float(ctx.eps), 1, _stream(h2.device)),
+                       "qt_rmsnorm_res")
+        shape = dn.shape if dn is not None else dh.shape
+        return dx.view(shape), (dx.view(shape) if ctx.has_y else None), dw.to(w.dtype), None
+
+
+def add_rmsnorm(x, y, norm: "RMSNorm"):
+    """(x + y, norm(x + y)) with the residual add fused into the norm's kernels (y None: (x, norm(x)) with the
+    residual gradient fused into the norm's backward)."""
+    d = x.shape[-1]
+    if _fused_norm_ok(d):
+        return _AddRMSNormFn.apply(x.to(torch.bfloat16), None if y is None else y.to(torch.bfloat16), norm.weight,
+                                   norm.eps)
+    h = x if y is None else x + y
+    return h, norm(h)
 
 
 class _RMSNormFn(torch.autograd.Function):
@@ -252,19 +313,21 @@ class Block(torch.nn.Module):
         self.q, self.k, self.v, self.o = ql(d, d, 0), ql(d, d, 1), ql(d, d, 2), ql(d, d, 3)
         self.gate, self.up, self.down = ql(d, h, 4), ql(d, h, 5), ql(h, d, 6)
 
-    def forward(self, x, cos, sin):  # x [B, S, d] bf16
+    def forward(self, x, cos, sin, y=None):
+        """x [B, S, d] bf16 residual stream; y: the previous block's pending branch output (added to x inside this
+        block's first norm).  Returns (h, y_out) with the block's output h + y_out; the add is left pending for
+        the next norm (LlamaQuartet.forward), so every residual add runs fused into an RMSNorm pass."""
         B, S, d = x.shape
         H, dh = self.n_head, d // self.n_head
-        a = self.attn_norm(x)
+        x, a = add_rmsnorm(x, y, self.attn_norm)
         q, k, v = linear_group(a, (self.q, self.k, self.v))  # one QuEST read of a for q/k/v
         q = rope(q.view(B, S, H, dh), cos, sin).transpose(1, 2)
         k = rope(k.view(B, S, H, dh), cos, sin).transpose(1, 2)
         v = v.view(B, S, H, dh).transpose(1, 2)
         att = F.scaled_dot_product_attention(q, k, v, is_causal=True)
-        x = x + self.o(att.transpose(1, 2).reshape(B, S, d))
-        m = self.mlp_norm(x)
+        x, m = add_rmsnorm(x, self.o(att.transpose(1, 2).reshape(B, S, d)), self.mlp_norm)
         g, u = linear_group(m, (self.gate, self.up))
-        return x + self.down(swiglu(g, u))
+        return x, self.down(swiglu(g, u))
 
 
 class LlamaQuartet(torch.nn.Module):
@@ -323,11 +386,12 @@ class LlamaQuartet(torch.nn.Module):
             self._launch_seeds()
         if x is None:
             x = F.embedding(tokens, self.embed).to(torch.bfloat16)
+        y = None
         for blk in self.blocks:
-            x = blk(x, self.cos, self.sin)
+            x, y = blk(x, self.cos, self.sin, y)
         if self.head is None:
-            return x
-        return self.head(self.norm(x))
+            return x + y
+        return self.head(add_rmsnorm(x, y, self.norm)[1])
 
 
 def lr_at(step: int, steps: int, lr: float, warmup_frac: float = 0.1, lr_floor: float = 0.0) -> float:

@@ -141,3 +141,51 @@ def test_fused_rope_strided_input(llama):
         a = llama._rope_call(xv, cos, sin, bwd)
         b = llama._rope_call(xv.contiguous(), cos, sin, bwd)
         assert torch.equal(a, b)
+
+
+def _unfused_logits(llama, model, tokens):
+    """The Llama forward with separate residual adds and norms (the structure before add_rmsnorm)."""
+    import torch.nn.functional as F
+
+    x = F.embedding(tokens, model.embed).to(torch.bfloat16)
+    for blk in model.blocks:
+        B, S, d = x.shape
+        H, dh = blk.n_head, d // blk.n_head
+        a = blk.attn_norm(x)
+        q, k, v = llama.linear_group(a, (blk.q, blk.k, blk.v))
+        q = llama.rope(q.view(B, S, H, dh), model.cos, model.sin).transpose(1, 2)
+        k = llama.rope(k.view(B, S, H, dh), model.cos, model.sin).transpose(1, 2)
+        v = v.view(B, S, H, dh).transpose(1, 2)
+        att = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+        x = x + blk.o(att.transpose(1, 2).reshape(B, S, d))
+        m = blk.mlp_norm(x)
+        g, u = llama.linear_group(m, (blk.gate, blk.up))
+        x = x + blk.down(llama.swiglu(g, u))
+    return model.head(model.norm(x))
+
+
+@pytest.mark.parametrize("linear", ["quartet", "bf16"])
+@pytest.mark.parametrize("d", [256, 4096])
+def test_fused_residual_norms_bit_identical(llama, linear, d):
+    """add_rmsnorm (residual add fused into the RMSNorm forward, the residual gradient into its backward;
+    qt_rmsnorm_res) gives the same loss and the same gradients, bit for bit, as separate adds and norms with
+    autograd's accumulation.  RMSNorm weight gradients are compared within fp32 rounding: their cross-block
+    atomic sums have no fixed order in either structure."""
+    cfg = llama.LlamaConfig(n_layer=2, d_model=d, n_head=d // 128, vocab=1024, seq_len=64, linear=linear)
+    model = llama.LlamaQuartet(cfg, seed=3, device="cuda")
+    model.eval()   # fixed backward seeds: both passes draw the same signs
+    tok, tgt = llama.synthetic_batch(cfg, 2, seed=1, device="cuda")
+    grads = []
+    for fwd in (lambda: model(tok), lambda: _unfused_logits(llama, model, tok)):
+        model.zero_grad(set_to_none=True)
+        logits = fwd()
+        loss = llama.cross_entropy(logits.reshape(-1, cfg.vocab), tgt.reshape(-1))
+        loss.backward()
+        grads.append((loss.detach().clone(), {n: p.grad.clone() for n, p in model.named_parameters()}))
+    (l0, g0), (l1, g1) = grads
+    assert torch.equal(l0, l1)
+    for n in g0:
+        if n.endswith("norm.weight"):
+            torch.testing.assert_close(g0[n], g1[n], rtol=1e-5, atol=1e-6)
+        else:
+            assert torch.equal(g0[n], g1[n]), n
