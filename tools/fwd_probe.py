@@ -20,7 +20,8 @@ def t(f, n=10):
 fb = torch.zeros(3, dtype=torch.int32, device="cuda")
 f = lambda: quant_fused(x, Q, RTN, transform=H, col_transform=RT, col_signs=s)  # noqa: E731
 for mode, name in ((3, "tc full (QuEST+RTN)"), (3 | 4 << 4, "hybrid: exact rows"), (3 | 1 << 4, "tc full, no QuEST"),
-                   (3 | 2 << 4, "tc full, no col RTN"), (3 | 3 << 4, "tc full, skeleton"), (0, "cuda-core fused")):
+                   (3 | 2 << 4, "tc full, no col RTN"), (3 | 3 << 4, "tc full, skeleton"), (0, "production (= tc full)"),
+                   (1, "cuda-core fused")):
     L.qt_debug_set_quant(mode, None)
     us = t(f)
     fb.zero_()
