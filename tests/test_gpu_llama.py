@@ -189,3 +189,28 @@ def test_fused_residual_norms_bit_identical(llama, linear, d):
             torch.testing.assert_close(g0[n], g1[n], rtol=1e-5, atol=1e-6)
         else:
             assert torch.equal(g0[n], g1[n]), n
+
+
+@pytest.mark.parametrize("d", [640, 1280, 1800, 2048, 6144])
+def test_add_rmsnorm_equals_add_then_norm(llama, d):
+    """qt_rmsnorm_res at the narrow (one warp per row, every NV) and wide kernel sizes: forward (h, n) equal
+    torch's bf16 add and the plain RMSNorm of it, backward dx equals the plain backward plus the residual
+    gradient (bf16 add), bit for bit; dw within fp32 rounding (atomic order)."""
+    g = torch.Generator(device="cuda").manual_seed(d)
+    x = torch.randn(777, d, device="cuda", generator=g).to(torch.bfloat16).requires_grad_(True)
+    y = torch.randn(777, d, device="cuda", generator=g).to(torch.bfloat16).requires_grad_(True)
+    norm = llama.RMSNorm(d, device="cuda")
+    with torch.no_grad():
+        norm.weight.uniform_(0.5, 1.5)
+    h, n = llama.add_rmsnorm(x, y, norm)
+    h_ref = x.detach() + y.detach()
+    assert torch.equal(h, h_ref)
+    h_ref.requires_grad_(True)
+    n_ref = norm(h_ref)
+    assert torch.equal(n, n_ref)
+    dh, dn = torch.randn_like(h), torch.randn_like(n)
+    dx, dy_, dw = torch.autograd.grad((h, n), (x, y, norm.weight), (dh, dn))
+    dh_ref, dw_ref = torch.autograd.grad(n_ref, (h_ref, norm.weight), dn)
+    assert torch.equal(dx, dh_ref + dh) and torch.equal(dy_, dx)
+    # dw: 777-term fp32 sums of O(1) products in different (atomic) orders: |error| <= 777 * 3 * 2^-24 ~ 1.4e-4
+    torch.testing.assert_close(dw, dw_ref, rtol=1e-5, atol=5e-4)

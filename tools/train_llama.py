@@ -59,10 +59,34 @@ def run(llama, preset, batch, steps, warmup, block, dev, world=1, rank=0, linear
         x = (torch.randn(batch, cfg.seq_len, cfg.d_model, device=dev) * 0.5).to(torch.bfloat16).requires_grad_()
         params = list(model.parameters())
 
-        def step(i):
+        def body():
             y = model(x=x)
             y.float().square().mean().backward()
+
+        def step(i):
+            body()
             return None
+
+        if graph:   # as Trainer(graph=True): device-resident layer seeds, two eager warm-ups, one captured fwd+bwd
+            if hasattr(model, "use_device_seeds"):
+                model.use_device_seeds()
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                for _ in range(2):
+                    for p in params + [x]:
+                        p.grad = None
+                    body()
+            torch.cuda.current_stream().wait_stream(st)
+            for p in params + [x]:
+                p.grad = None
+            cg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(cg):
+                body()
+
+            def step(i):
+                cg.replay()
+                return None
     else:
         tr = llama.Trainer(model, steps=1000, lr=llama.PAPER_LR[preset], graph=graph)
         tok, tgt = llama.synthetic_batch(cfg, batch, seed=rank, device=dev)
@@ -87,7 +111,8 @@ def run(llama, preset, batch, steps, warmup, block, dev, world=1, rank=0, linear
         ms = float(t.item())
     lin = cfg.n_layer * (4 * cfg.d_model ** 2 + 3 * cfg.d_model * cfg.hidden) + (0 if block else cfg.d_model * cfg.vocab)
     out = {"preset": preset, "linear": linear, "block_only": block, "n_layer": cfg.n_layer, "d_model": cfg.d_model,
-           "launch": "eager" if block or not graph else "CUDA graph of the whole training step",
+           "launch": ("CUDA graph of the whole training step" if not block else "CUDA graph of the block's fwd+bwd")
+           if graph else "eager",
            "seq_len": cfg.seq_len, "seqs_per_gpu": batch, "n_gpus": world, "ms_per_step": round(ms, 3),
            "tokens_per_s": round(world * tokens / (ms * 1e-3), 1),
            "linear_tflops": round(world * 6 * tokens * lin / (ms * 1e-3) / 1e12, 1)}
