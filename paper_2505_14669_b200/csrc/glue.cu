@@ -460,6 +460,10 @@ QT_API int qt_rmsnorm_res(const void* x, const void* res, const float* w, const 
         int blocks = grid_for(rows * 256);
         if (blocks > 1184) blocks = 1184;
         auto wide = [&](auto kern) {
+            int per_sm = 0;   // backward: one wave of resident blocks (one dw atomic per column per block)
+            if (backward && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0) == cudaSuccess &&
+                per_sm > 0)
+                blocks = std::min<int>(blocks, per_sm * (int)qt::device_sms());
             kern<<<blocks, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint4*>(x), w, static_cast<const uint4*>(dy),
                                                            static_cast<uint4*>(out), rstd, dw, rows, eps, backward,
                                                            static_cast<const uint4*>(res), static_cast<uint4*>(h_out));
